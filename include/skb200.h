@@ -1,0 +1,167 @@
+/*
+ * skb200.h -- C ABI of the B200-native Stream-K GEMM (libskb200.so).
+ *
+ * This is the drop-in boundary for the reference's GEMM hot path
+ * (/root/reference/proj, "streamk-lab"):
+ *
+ *   reference (C++ templates, header-only)         this ABI (extern "C", POD only)
+ *   -----------------------------------------------------------------------------
+ *   tile_grid            types.cpp:45-55            sk_tile_grid
+ *   iter_to_coords       types.cpp:57-62            sk_iter_to_coords
+ *   data_parallel / fixed_split / stream_k / hybrid
+ *                        decompose.cpp:38-121       sk_schedule
+ *   fixup_peers_of       decompose.cpp:123-136      sk_fixup_peers
+ *   quantization_efficiency decompose.cpp:138-141   sk_quantization_efficiency
+ *   execute<T>(assignment, A, B, threads)
+ *                        executor.hpp:130-207       sk_execute   (host buffers, synchronous)
+ *                                                   sk_gemm      (device buffers, stream-ordered)
+ *   detail::FixupStore   executor.hpp:95-119        sk_workspace_size / sk_workspace_init /
+ *                                                   sk_workspace_check (device fixup slabs + flags)
+ *
+ * Conventions mirror the reference: row-major A (m x k), B (k x n), C (m x n);
+ * tiles linearised row-major over (tiles_m, tiles_n); C = A * B with alpha/beta
+ * ignored exactly as executor.hpp:142,179 ignores them.  Exceptions become status
+ * codes: std::invalid_argument -> SK_EINVAL, std::out_of_range -> SK_ERANGE,
+ * std::logic_error (double signal) -> SK_EPROTOCOL.  No C++ types cross the ABI.
+ *
+ * Threading: every entry point is reentrant.  Per-device state (SM count, kernel
+ * attributes) is initialised lazily under a mutex; sk_execute keeps one
+ * device-buffer cache per host thread.  Workspaces belong to the caller.
+ */
+#ifndef SKB200_H_
+#define SKB200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SKB200_ABI_VERSION 1
+
+typedef enum sk_status {
+  SK_OK = 0,
+  SK_EINVAL = 1,        /* std::invalid_argument in the reference */
+  SK_EUNSUPPORTED = 2,  /* valid for the reference, not for this kernel (blocking, alignment) */
+  SK_ECUDA = 3,         /* CUDA runtime / driver error; see sk_last_error() */
+  SK_EPROTOCOL = 4,     /* fixup protocol violation: double signal or wait watchdog */
+  SK_ERANGE = 5,        /* std::out_of_range (iter_to_coords) */
+  SK_ECAPACITY = 6      /* caller buffer too small; the required size is still reported */
+} sk_status;
+
+/* Strategy tags: types.hpp:70 Strategy / decompose.hpp:9 HybridVariant. */
+typedef enum sk_strategy {
+  SK_DATA_PARALLEL = 0,
+  SK_FIXED_SPLIT = 1,   /* param = s */
+  SK_STREAM_K = 2,      /* param = g */
+  SK_DP_ONE_TILE_SK = 3, /* param = p */
+  SK_TWO_TILE_SK_DP = 4  /* param = p */
+} sk_strategy;
+
+typedef enum sk_dtype {
+  SK_INT64 = 0,    /* reference DType::Int64 (CPU-only in the reference; no device kernel) */
+  SK_FLOAT32 = 1,  /* reference DType::Float32 */
+  SK_FLOAT64 = 2,  /* reference DType::Float64 */
+  SK_BFLOAT16 = 3, /* tensor-core input types (accumulate and store in FLOAT32) */
+  SK_FLOAT16 = 4
+} sk_dtype;
+
+/* Kernel family: one tile configuration per precision. */
+typedef enum sk_variant {
+  SK_VARIANT_AUTO = 0,
+  SK_VARIANT_1SM = 1, /* BF16/FP16: 128x256x64, tcgen05 cta_group::1, persistent grid = #SMs */
+  SK_VARIANT_2SM = 2  /* BF16/FP16: 256x256x64, tcgen05 cta_group::2, persistent grid = #SMs/2 pairs */
+} sk_variant;
+
+/* types.hpp:20-27.  alpha/beta carried but ignored (executor.hpp:142,179). */
+typedef struct sk_problem {
+  int64_t m, n, k;
+  double alpha, beta;
+} sk_problem;
+
+/* types.hpp:30-34 */
+typedef struct sk_blocking {
+  int64_t blk_m, blk_n, blk_k;
+} sk_blocking;
+
+/* types.hpp:41-47 */
+typedef struct sk_tile_grid_t {
+  int64_t tiles_m, tiles_n, total_tiles, iters_per_tile, total_iters;
+} sk_tile_grid_t;
+
+/* Device GEMM descriptor for sk_gemm.  All pointers are device pointers owned
+ * by the caller; leading dimensions are in elements. */
+typedef struct sk_gemm_desc {
+  sk_problem problem;
+  sk_blocking blocking; /* must equal sk_kernel_blocking(ab_type, variant) */
+  int32_t strategy;     /* sk_strategy */
+  int32_t ab_type;      /* SK_BFLOAT16 | SK_FLOAT16 | SK_FLOAT64 */
+  int64_t param;        /* s, g or p (ignored for data_parallel) */
+  int32_t variant;      /* sk_variant */
+  int32_t num_ctas;     /* persistent CTAs (pairs for 2-SM); 0 = all SMs */
+  const void* A;
+  int64_t lda;          /* >= k, lda * sizeof(ab) % 16 == 0 */
+  const void* B;
+  int64_t ldb;          /* >= n, ldb * sizeof(ab) % 16 == 0 */
+  void* C;              /* FLOAT32 for BF16/FP16 inputs, FLOAT64 for FP64 */
+  int64_t ldc;          /* >= n, ldc * sizeof(c) % 16 == 0 */
+  int32_t* trace;       /* optional device buffer, see sk_trace_size(); NULL = off */
+} sk_gemm_desc;
+
+const char* sk_status_string(sk_status status);
+/* Thread-local detail string for the last non-OK status on this thread. */
+const char* sk_last_error(void);
+int sk_abi_version(void);
+
+/* ---- integer schedule (host, closed form; bit-exact with decompose.cpp) ---- */
+sk_status sk_tile_grid(const sk_problem* problem, const sk_blocking* blocking,
+                       sk_tile_grid_t* out);
+sk_status sk_iter_to_coords(const sk_tile_grid_t* grid, int64_t i, int64_t* tile_idx,
+                            int64_t* local_iter);
+/* Writes the grid size to *grid_size and, when ranges != NULL and capacity >= g,
+ * the [g][2] (iter_begin, iter_end) table; row index == cta_id. */
+sk_status sk_schedule(const sk_problem* problem, const sk_blocking* blocking,
+                      sk_strategy strategy, int64_t param, int64_t* grid_size, int64_t* ranges,
+                      int64_t capacity);
+/* fixup_peers_of as CSR: offsets[total_tiles + 1], ids[nnz] ascending per tile.
+ * ids may be NULL to query *nnz. */
+sk_status sk_fixup_peers(const sk_problem* problem, const sk_blocking* blocking,
+                         sk_strategy strategy, int64_t param, int64_t* offsets, int64_t* ids,
+                         int64_t capacity, int64_t* nnz);
+sk_status sk_quantization_efficiency(int64_t t, int64_t p, double* out);
+
+/* ---- device GEMM -------------------------------------------------------- */
+/* The tile configuration the device kernel uses for an input type/variant. */
+sk_status sk_kernel_blocking(sk_dtype ab_type, sk_variant variant, sk_blocking* out);
+/* Bytes of device workspace (fixup flags + fp32/fp64 partial slabs). */
+sk_status sk_workspace_size(const sk_gemm_desc* desc, size_t* bytes);
+/* Zero a workspace once after allocation (stream-ordered).  The kernel leaves
+ * it zeroed again after every successful launch (self-cleaning flags). */
+sk_status sk_workspace_init(void* workspace, size_t bytes, void* stream);
+/* Synchronises the stream, reads and clears the workspace error word. */
+sk_status sk_workspace_check(void* workspace, void* stream);
+/* Ints needed for the optional ownership trace: per tile {owner, last_peer,
+ * storing_unit, segments} followed by per unit {partials_emitted}. */
+sk_status sk_trace_size(const sk_gemm_desc* desc, int64_t* ints);
+/* Stream-ordered, asynchronous.  Does not synchronise. */
+sk_status sk_gemm(const sk_gemm_desc* desc, void* workspace, size_t workspace_bytes,
+                  void* stream);
+
+/* ---- reference-facing drop-in of streamk::execute<T> ------------------- */
+/* Host buffers in, host C out (tight row-major, ld = cols), synchronous.
+ * host_type: SK_BFLOAT16 / SK_FLOAT16 (raw 16-bit), SK_FLOAT32 (values rounded
+ * to compute_type on the device), SK_FLOAT64 (compute_type must be FLOAT64).
+ * C is float32 for 16-bit compute, float64 for FP64.  Device buffers, workspace
+ * and the stream are cached per host thread.  device < 0 = current device. */
+sk_status sk_execute(const sk_problem* problem, const sk_blocking* blocking,
+                     sk_strategy strategy, int64_t param, sk_dtype host_type,
+                     sk_dtype compute_type, int32_t variant, const void* A, const void* B,
+                     void* C, int32_t device);
+/* Releases the calling thread's sk_execute cache. */
+void sk_execute_release(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SKB200_H_ */

@@ -1,0 +1,504 @@
+"""paper_2301_03598_b200 -- B200-native Stream-K GEMM behind the reference's API.
+
+Python mirror of the reference core's public surface (/root/reference/proj,
+core/include/streamk/*.hpp), implemented entirely by the C-ABI library
+``_lib/libskb200.so`` (include/skb200.h): schedules are computed by its C++
+closed forms, GEMMs run in its hand-written sm_100a kernels.  There is no
+Python or CPU fallback: if the library is missing every entry point raises.
+
+    reference                               here
+    ---------------------------------------------------------------------------
+    GemmProblem / BlockingFactors            GemmProblem / BlockingFactors
+    tile_grid / iter_to_coords               tile_grid / iter_to_coords
+    data_parallel / fixed_split /            data_parallel / fixed_split /
+      stream_k / hybrid                        stream_k / hybrid
+    fixup_peers_of / quantization_efficiency fixup_peers_of / quantization_efficiency
+    to_text / from_text                      to_text / from_text
+    execute<T>(a, A, B, threads)             execute(a, A, B)  (host arrays in/out)
+                                             Gemm(a, ...).run(A, B, C) (device tensors)
+
+Exceptions follow the reference: std::invalid_argument -> ValueError,
+std::out_of_range -> IndexError, std::logic_error (double signal) ->
+ProtocolError (a RuntimeError).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import os
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libskb200.so")
+
+__all__ = [
+    "DType", "Strategy", "HybridVariant", "Variant", "GemmProblem", "BlockingFactors", "TileGrid",
+    "TileCoords", "CtaRange", "WorkAssignment", "tile_grid", "iter_to_coords", "data_parallel",
+    "fixed_split", "stream_k", "hybrid", "fixup_peers_of", "quantization_efficiency", "to_text",
+    "from_text", "kernel_blocking", "execute", "Gemm", "ProtocolError", "UnsupportedError",
+    "CudaError", "lib",
+]
+
+
+# ----------------------------------------------------------------------------- errors
+class ProtocolError(RuntimeError):
+    """std::logic_error in the reference: a fixup flag signalled twice (or the
+    device wait watchdog fired)."""
+
+
+class UnsupportedError(RuntimeError):
+    """Valid for the reference, not for this device kernel (tile config, alignment)."""
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+SK_OK, SK_EINVAL, SK_EUNSUPPORTED, SK_ECUDA, SK_EPROTOCOL, SK_ERANGE, SK_ECAPACITY = range(7)
+
+
+# ----------------------------------------------------------------------------- C ABI
+class sk_problem(C.Structure):
+    _fields_ = [("m", C.c_int64), ("n", C.c_int64), ("k", C.c_int64), ("alpha", C.c_double),
+                ("beta", C.c_double)]
+
+
+class sk_blocking(C.Structure):
+    _fields_ = [("blk_m", C.c_int64), ("blk_n", C.c_int64), ("blk_k", C.c_int64)]
+
+
+class sk_tile_grid_t(C.Structure):
+    _fields_ = [("tiles_m", C.c_int64), ("tiles_n", C.c_int64), ("total_tiles", C.c_int64),
+                ("iters_per_tile", C.c_int64), ("total_iters", C.c_int64)]
+
+
+class sk_gemm_desc(C.Structure):
+    _fields_ = [
+        ("problem", sk_problem), ("blocking", sk_blocking), ("strategy", C.c_int32),
+        ("ab_type", C.c_int32), ("param", C.c_int64), ("variant", C.c_int32),
+        ("num_ctas", C.c_int32), ("A", C.c_void_p), ("lda", C.c_int64), ("B", C.c_void_p),
+        ("ldb", C.c_int64), ("C", C.c_void_p), ("ldc", C.c_int64),
+        ("trace", C.c_void_p),
+    ]
+
+
+_P = C.POINTER
+_lib: Optional[C.CDLL] = None
+
+_SIGS = {
+    "sk_status_string": (C.c_char_p, [C.c_int]),
+    "sk_last_error": (C.c_char_p, []),
+    "sk_abi_version": (C.c_int, []),
+    "sk_tile_grid": (C.c_int, [_P(sk_problem), _P(sk_blocking), _P(sk_tile_grid_t)]),
+    "sk_iter_to_coords": (C.c_int, [_P(sk_tile_grid_t), C.c_int64, _P(C.c_int64), _P(C.c_int64)]),
+    "sk_schedule": (C.c_int, [_P(sk_problem), _P(sk_blocking), C.c_int, C.c_int64, _P(C.c_int64),
+                              C.c_void_p, C.c_int64]),
+    "sk_fixup_peers": (C.c_int, [_P(sk_problem), _P(sk_blocking), C.c_int, C.c_int64, C.c_void_p,
+                                 C.c_void_p, C.c_int64, _P(C.c_int64)]),
+    "sk_quantization_efficiency": (C.c_int, [C.c_int64, C.c_int64, _P(C.c_double)]),
+    "sk_kernel_blocking": (C.c_int, [C.c_int, C.c_int, _P(sk_blocking)]),
+    "sk_workspace_size": (C.c_int, [_P(sk_gemm_desc), _P(C.c_size_t)]),
+    "sk_workspace_init": (C.c_int, [C.c_void_p, C.c_size_t, C.c_void_p]),
+    "sk_workspace_check": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "sk_trace_size": (C.c_int, [_P(sk_gemm_desc), _P(C.c_int64)]),
+    "sk_gemm": (C.c_int, [_P(sk_gemm_desc), C.c_void_p, C.c_size_t, C.c_void_p]),
+    "sk_execute": (C.c_int, [_P(sk_problem), _P(sk_blocking), C.c_int, C.c_int64, C.c_int, C.c_int,
+                             C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32]),
+    "sk_execute_release": (None, []),
+}
+
+
+def lib() -> C.CDLL:
+    """Load libskb200.so (built by paper_2301_03598_b200.build / __graft_entry__.build)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_2301_03598_b200.build`"
+                              " (there is no CPU fallback)")
+        h = C.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            f = getattr(h, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = h
+    return _lib
+
+
+def _check(st: int, what: str = "") -> None:
+    if st == SK_OK:
+        return
+    detail = lib().sk_last_error().decode()
+    msg = f"{what}: {detail}" if what else detail
+    if st == SK_EINVAL:
+        raise ValueError(msg)
+    if st == SK_ERANGE:
+        raise IndexError(msg)
+    if st == SK_EPROTOCOL:
+        raise ProtocolError(msg)
+    if st == SK_EUNSUPPORTED:
+        raise UnsupportedError(msg)
+    if st == SK_ECUDA:
+        raise CudaError(msg)
+    raise RuntimeError(f"{msg} (status {st})")
+
+
+# ----------------------------------------------------------------------------- domain (types.hpp)
+class DType(enum.IntEnum):
+    Int64 = 0
+    Float32 = 1
+    Float64 = 2
+    BFloat16 = 3
+    Float16 = 4
+
+
+class Strategy(enum.IntEnum):  # types.hpp:70
+    DataParallel = 0
+    FixedSplit = 1
+    StreamK = 2
+    DpOneTileSk = 3
+    TwoTileSkDp = 4
+
+
+class HybridVariant(enum.IntEnum):  # decompose.hpp:9
+    DpOneTileSk = 3
+    TwoTileSkDp = 4
+
+
+class Variant(enum.IntEnum):
+    Auto = 0
+    OneSM = 1
+    TwoSM = 2
+
+
+_STRATEGY_NAMES = {
+    Strategy.DataParallel: "data_parallel", Strategy.FixedSplit: "fixed_split",
+    Strategy.StreamK: "stream_k", Strategy.DpOneTileSk: "dp_one_tile_sk",
+    Strategy.TwoTileSkDp: "two_tile_sk_dp",
+}
+
+
+def strategy_name(s: Strategy) -> str:  # types.cpp:64-73
+    return _STRATEGY_NAMES[Strategy(s)]
+
+
+@dataclass(frozen=True)
+class GemmProblem:  # types.hpp:20-27
+    m: int = 1
+    n: int = 1
+    k: int = 1
+    alpha: float = 1.0
+    beta: float = 0.0
+    dtype: DType = DType.Float32
+
+    def _c(self) -> sk_problem:
+        return sk_problem(self.m, self.n, self.k, self.alpha, self.beta)
+
+
+@dataclass(frozen=True)
+class BlockingFactors:  # types.hpp:30-34
+    blk_m: int = 1
+    blk_n: int = 1
+    blk_k: int = 1
+
+    def _c(self) -> sk_blocking:
+        return sk_blocking(self.blk_m, self.blk_n, self.blk_k)
+
+
+@dataclass(frozen=True)
+class TileGrid:  # types.hpp:41-47
+    tiles_m: int = 0
+    tiles_n: int = 0
+    total_tiles: int = 0
+    iters_per_tile: int = 0
+    total_iters: int = 0
+
+    def _c(self) -> sk_tile_grid_t:
+        return sk_tile_grid_t(self.tiles_m, self.tiles_n, self.total_tiles, self.iters_per_tile,
+                              self.total_iters)
+
+
+@dataclass(frozen=True)
+class TileCoords:
+    tile_idx: int
+    local_iter: int
+
+
+@dataclass(frozen=True)
+class CtaRange:  # types.hpp:61-68
+    cta_id: int
+    iter_begin: int
+    iter_end: int
+
+    def length(self) -> int:
+        return self.iter_end - self.iter_begin
+
+    def empty(self) -> bool:
+        return self.iter_end == self.iter_begin
+
+
+@dataclass
+class WorkAssignment:  # types.hpp:76-84
+    strategy: Strategy = Strategy.DataParallel
+    grid_size: int = 0
+    split: int = 1
+    problem: GemmProblem = field(default_factory=GemmProblem)
+    blocking: BlockingFactors = field(default_factory=BlockingFactors)
+    grid: TileGrid = field(default_factory=TileGrid)
+    ranges: List[CtaRange] = field(default_factory=list)
+    # The decomposition knob the closed-form device scheduler needs (s, g or p).
+    param: int = 1
+
+    def range_table(self) -> np.ndarray:
+        return np.array([[r.iter_begin, r.iter_end] for r in self.ranges], np.int64).reshape(-1, 2)
+
+
+def tile_grid(problem: GemmProblem, blocking: BlockingFactors) -> TileGrid:  # types.cpp:45-55
+    out = sk_tile_grid_t()
+    _check(lib().sk_tile_grid(C.byref(problem._c()), C.byref(blocking._c()), C.byref(out)),
+           "tile_grid")
+    return TileGrid(out.tiles_m, out.tiles_n, out.total_tiles, out.iters_per_tile, out.total_iters)
+
+
+def iter_to_coords(grid: TileGrid, i: int) -> TileCoords:  # types.cpp:57-62
+    t, l = C.c_int64(), C.c_int64()
+    _check(lib().sk_iter_to_coords(C.byref(grid._c()), i, C.byref(t), C.byref(l)),
+           "iter_to_coords")
+    return TileCoords(t.value, l.value)
+
+
+def _schedule_table(problem, blocking, strategy: Strategy, param: int) -> np.ndarray:
+    g = C.c_int64()
+    p, b = problem._c(), blocking._c()
+    _check(lib().sk_schedule(C.byref(p), C.byref(b), int(strategy), param, C.byref(g), None, 0),
+           strategy_name(strategy))
+    tbl = np.zeros((g.value, 2), np.int64)
+    _check(lib().sk_schedule(C.byref(p), C.byref(b), int(strategy), param, C.byref(g),
+                             tbl.ctypes.data_as(C.c_void_p), g.value), strategy_name(strategy))
+    return tbl
+
+
+def _assignment(strategy: Strategy, problem: GemmProblem, blocking: BlockingFactors,
+                param: int) -> WorkAssignment:
+    tbl = _schedule_table(problem, blocking, strategy, param)
+    return WorkAssignment(
+        strategy=strategy, grid_size=tbl.shape[0],
+        split=param if strategy == Strategy.FixedSplit else 1, problem=problem, blocking=blocking,
+        grid=tile_grid(problem, blocking),
+        ranges=[CtaRange(i, int(b), int(e)) for i, (b, e) in enumerate(tbl)], param=param)
+
+
+def data_parallel(problem: GemmProblem, blocking: BlockingFactors) -> WorkAssignment:
+    return _assignment(Strategy.DataParallel, problem, blocking, 1)  # decompose.cpp:38-48
+
+
+def fixed_split(problem: GemmProblem, blocking: BlockingFactors, s: int) -> WorkAssignment:
+    return _assignment(Strategy.FixedSplit, problem, blocking, s)  # decompose.cpp:50-69
+
+
+def stream_k(problem: GemmProblem, blocking: BlockingFactors, g: int) -> WorkAssignment:
+    return _assignment(Strategy.StreamK, problem, blocking, g)  # decompose.cpp:71-79
+
+
+def hybrid(problem: GemmProblem, blocking: BlockingFactors, p: int,
+           variant: HybridVariant) -> WorkAssignment:  # decompose.cpp:81-121
+    return _assignment(Strategy(int(variant)), problem, blocking, p)
+
+
+def fixup_peers_of(a: WorkAssignment) -> List[List[int]]:  # decompose.cpp:123-136
+    off, ids = _peers_csr(a)
+    return [ids[off[t]:off[t + 1]].tolist() for t in range(a.grid.total_tiles)]
+
+
+def _peers_csr(a: WorkAssignment):
+    p, b = a.problem._c(), a.blocking._c()
+    off = np.zeros(a.grid.total_tiles + 1, np.int64)
+    nnz = C.c_int64()
+    _check(lib().sk_fixup_peers(C.byref(p), C.byref(b), int(a.strategy), a.param,
+                                off.ctypes.data_as(C.c_void_p), None, 0, C.byref(nnz)),
+           "fixup_peers_of")
+    ids = np.zeros(max(nnz.value, 1), np.int64)
+    _check(lib().sk_fixup_peers(C.byref(p), C.byref(b), int(a.strategy), a.param,
+                                off.ctypes.data_as(C.c_void_p), ids.ctypes.data_as(C.c_void_p),
+                                ids.size, C.byref(nnz)), "fixup_peers_of")
+    return off, ids[: nnz.value]
+
+
+def quantization_efficiency(t: int, p: int) -> float:  # decompose.cpp:138-141
+    out = C.c_double()
+    _check(lib().sk_quantization_efficiency(t, p, C.byref(out)), "quantization_efficiency")
+    return out.value
+
+
+# ----------------------------------------------------------------------------- text form
+def to_text(a: WorkAssignment) -> str:  # types.cpp:96-107
+    lines = [f"{a.problem.m} {a.problem.n} {a.problem.k}",
+             f"{a.blocking.blk_m} {a.blocking.blk_n} {a.blocking.blk_k}"]
+    tok = strategy_name(a.strategy)
+    if a.strategy == Strategy.FixedSplit:
+        tok += f":{a.split}"
+    lines.append(f"{tok} {a.grid_size}")
+    lines += [f"{r.cta_id} {r.iter_begin} {r.iter_end}" for r in a.ranges]
+    return "\n".join(lines) + "\n"
+
+
+def from_text(text: str) -> WorkAssignment:  # types.cpp:109-128
+    toks = text.split()
+    try:
+        m, n, k = (int(x) for x in toks[0:3])
+        bm, bn, bk = (int(x) for x in toks[3:6])
+        tok, g = toks[6], int(toks[7])
+    except (IndexError, ValueError) as e:
+        raise ValueError("assignment text: bad header") from e
+    split = 1
+    if tok.startswith("fixed_split:"):
+        split = int(tok[len("fixed_split:"):])
+        strategy = Strategy.FixedSplit
+    else:
+        inv = {v: k_ for k_, v in _STRATEGY_NAMES.items()}
+        if tok not in inv:
+            raise ValueError("unknown strategy token: " + tok)
+        strategy = inv[tok]
+    rest = toks[8:]
+    ranges = [CtaRange(int(rest[i]), int(rest[i + 1]), int(rest[i + 2]))
+              for i in range(0, len(rest) - len(rest) % 3, 3)]
+    if len(ranges) != g:
+        raise ValueError("assignment text: range count != grid size")
+    problem, blocking = GemmProblem(m, n, k), BlockingFactors(bm, bn, bk)
+    a = WorkAssignment(strategy=strategy, grid_size=g, split=split, problem=problem,
+                       blocking=blocking, grid=tile_grid(problem, blocking), ranges=ranges)
+    a.param = _infer_param(a)
+    return a
+
+
+def _infer_param(a: WorkAssignment) -> int:
+    """Recover the closed-form knob (s, g or p) of a parsed assignment; 0 when
+    the range table is not one the device scheduler can reproduce."""
+    want = a.range_table()
+    if a.strategy == Strategy.DataParallel:
+        cands = [1]
+    elif a.strategy == Strategy.FixedSplit:
+        cands = [a.split]
+    elif a.strategy == Strategy.StreamK:
+        cands = [a.grid_size]
+    else:
+        cands = range(1, a.grid_size + 1)
+    for c in cands:
+        try:
+            tbl = _schedule_table(a.problem, a.blocking, a.strategy, c)
+        except ValueError:
+            continue
+        if tbl.shape == want.shape and np.array_equal(tbl, want):
+            return c
+    return 0
+
+
+# ----------------------------------------------------------------------------- device GEMM
+def kernel_blocking(ab_type: DType = DType.BFloat16, variant: Variant = Variant.Auto) -> BlockingFactors:
+    """The single tile configuration per precision the device kernel uses."""
+    out = sk_blocking()
+    _check(lib().sk_kernel_blocking(int(ab_type), int(variant), C.byref(out)), "kernel_blocking")
+    return BlockingFactors(out.blk_m, out.blk_n, out.blk_k)
+
+
+def _host_type(arr: np.ndarray) -> DType:
+    if arr.dtype == np.float32:
+        return DType.Float32
+    if arr.dtype == np.float64:
+        return DType.Float64
+    if arr.dtype == np.float16:
+        return DType.Float16
+    if arr.dtype == np.uint16:  # raw bfloat16 bits
+        return DType.BFloat16
+    raise ValueError(f"unsupported host dtype {arr.dtype}")
+
+
+def execute(a: WorkAssignment, A: np.ndarray, B: np.ndarray, compute: DType = DType.BFloat16,
+            variant: Variant = Variant.Auto, device: int = -1) -> np.ndarray:
+    """Drop-in of streamk::execute<T> (executor.hpp:130-207): host A (m x k),
+    B (k x n) in, new host C (m x n) out, synchronous.  A/B may be float32
+    (rounded to `compute` on the device), float16, uint16 (bfloat16 bits) or
+    float64 (compute must be Float64).  C is float32 (float64 for FP64)."""
+    p = a.problem
+    if A.shape != (p.m, p.k) or B.shape != (p.k, p.n):
+        raise ValueError("execute: matrix shapes do not match assignment")
+    if a.param == 0:
+        raise UnsupportedError("execute: range table is not a closed-form schedule")
+    ht = _host_type(A)
+    if _host_type(B) != ht:
+        raise ValueError("execute: A and B host dtypes differ")
+    A = np.ascontiguousarray(A)
+    B = np.ascontiguousarray(B)
+    Cm = np.empty((p.m, p.n), np.float64 if compute == DType.Float64 else np.float32)
+    _check(lib().sk_execute(C.byref(p._c()), C.byref(a.blocking._c()), int(a.strategy), a.param,
+                            int(ht), int(compute), int(variant), A.ctypes.data_as(C.c_void_p),
+                            B.ctypes.data_as(C.c_void_p), Cm.ctypes.data_as(C.c_void_p), device),
+           "execute")
+    return Cm
+
+
+class Gemm:
+    """A planned device GEMM (stream-ordered, device pointers): the
+    sk_gemm_desc plus its self-cleaning fixup workspace.
+
+    Tensors are torch CUDA tensors (torch is device-memory plumbing here, not
+    compute): A (m x k) and B (k x n) in bf16/fp16, C (m x n) fp32, each
+    row-major with a 16-byte-multiple leading dimension.
+    """
+
+    def __init__(self, a: WorkAssignment, ab_type: DType = DType.BFloat16,
+                 variant: Variant = Variant.Auto, num_ctas: int = 0, trace: bool = False):
+        import torch  # device memory only
+
+        if a.param == 0:
+            raise UnsupportedError("Gemm: range table is not a closed-form schedule")
+        self.a = a
+        self.ab_type = ab_type
+        d = sk_gemm_desc()
+        d.problem = a.problem._c()
+        d.blocking = a.blocking._c()
+        d.strategy = int(a.strategy)
+        d.ab_type = int(ab_type)
+        d.param = a.param
+        d.variant = int(variant)
+        d.num_ctas = num_ctas
+        d.lda, d.ldb, d.ldc = a.problem.k, a.problem.n, a.problem.n
+        self.desc = d
+        ws = C.c_size_t()
+        _check(lib().sk_workspace_size(C.byref(d), C.byref(ws)), "workspace_size")
+        self.ws_bytes = ws.value
+        self.workspace = torch.empty(max(self.ws_bytes, 256), dtype=torch.uint8, device="cuda")
+        stream = torch.cuda.current_stream().cuda_stream
+        _check(lib().sk_workspace_init(C.c_void_p(self.workspace.data_ptr()), self.ws_bytes,
+                                       C.c_void_p(stream)), "workspace_init")
+        self.trace = None
+        if trace:
+            n = C.c_int64()
+            _check(lib().sk_trace_size(C.byref(d), C.byref(n)), "trace_size")
+            self.trace = torch.full((n.value,), -1, dtype=torch.int32, device="cuda")
+            self.trace[4 * a.grid.total_tiles:] = 0
+
+    def run(self, A, B, Cout, stream=None) -> None:
+        import torch
+
+        d = self.desc
+        for t, name in ((A, "A"), (B, "B"), (Cout, "C")):
+            if not t.is_cuda or t.stride(1) != 1:
+                raise ValueError(f"{name} must be a row-major CUDA tensor")
+        d.A, d.lda = A.data_ptr(), A.stride(0)
+        d.B, d.ldb = B.data_ptr(), B.stride(0)
+        d.C, d.ldc = Cout.data_ptr(), Cout.stride(0)
+        d.trace = self.trace.data_ptr() if self.trace is not None else None
+        s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+        _check(lib().sk_gemm(C.byref(d), C.c_void_p(self.workspace.data_ptr()), self.ws_bytes,
+                             C.c_void_p(s)), "sk_gemm")
+
+    def check(self, stream=None) -> None:
+        """Synchronise and raise ProtocolError if the fixup protocol misbehaved."""
+        import torch
+
+        s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+        _check(lib().sk_workspace_check(C.c_void_p(self.workspace.data_ptr()), C.c_void_p(s)),
+               "workspace_check")

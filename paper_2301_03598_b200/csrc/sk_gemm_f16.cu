@@ -1,0 +1,305 @@
+// sk_gemm_f16.cu -- persistent, warp-specialised Stream-K GEMM for sm_100a.
+//
+// C (fp32, m x n) = A (bf16|fp16, m x k, row-major) * B (bf16|fp16, k x n, row-major)
+// under any of the reference's five decompositions (decompose.cpp:38-121).
+//
+// Replaces the reference executor (executor.hpp:130-207):
+//   mac_loop (executor.hpp:59-88)     -> TMA producer warp -> smem ring -> tcgen05.mma
+//                                        issuer, fp32 accumulator in TMEM
+//   FixupStore (executor.hpp:95-119)  -> fp32 slabs in global memory + int flags with
+//                                        release/acquire (sk_kernel_common.cuh)
+//   owner fold + StoreTile (:164-181) -> epilogue warps: TMEM -> regs (+ peer slabs in
+//                                        ascending id) -> swizzled smem -> TMA store
+//   worker loop (:187-193)            -> persistent grid, descending logical ids
+//
+// Warp roles (192 threads, 1 CTA per SM):
+//   warp 0      TMA producer (one lane)
+//   warp 1      TMEM allocator + tcgen05.mma issuer (one lane)
+//   warps 2..5  epilogue; warp w drains TMEM lanes 32*(w%4) .. +31
+//
+// Tile config (one per precision): 1-SM 128x256x64.
+// The smem ring holds STAGES k-blocks: A 128x64 (K-major, 128B swizzle, 16 KB)
+// and B 64x256 as four 64x64 boxes (MN-major, 128B swizzle, 32 KB).
+// TMEM: two 256-column fp32 accumulators, so the epilogue of one segment
+// overlaps the mainloop of the next.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "ptx.cuh"
+#include "schedule.hpp"
+#include "sk_kernel_common.cuh"
+
+namespace skb200 {
+namespace f16 {
+
+constexpr int BM = 128;  // rows per CTA (per TMEM accumulator)
+constexpr int BN = 256;
+constexpr int BK = 64;
+constexpr int UMMA_K = 16;
+constexpr int STAGES = 4;
+constexpr int A_STAGE_BYTES = BM * BK * 2;           // 16 KB
+constexpr int B_BOX_BYTES = 64 * BK * 2;             // 8 KB: 64 k-rows x 64 n
+constexpr int B_STAGE_BYTES = BN * BK * 2;           // 32 KB
+constexpr int EPI_WARPS = 4;
+constexpr int EPI_BUF_BYTES = 32 * 32 * 4;           // 32 rows x 32 fp32 = 4 KB
+constexpr int EPI_BYTES = EPI_WARPS * 2 * EPI_BUF_BYTES;  // 32 KB
+constexpr int NUM_THREADS = 64 + 32 * EPI_WARPS;     // 192
+constexpr int TMEM_COLS = 512;                       // 2 x 256-col accumulators
+constexpr int SLAB_ELEMS = BM * BN;                  // fp32 partial per CTA rank
+
+struct SmemLayout {
+  static constexpr int a_off = 0;
+  static constexpr int b_off = a_off + STAGES * A_STAGE_BYTES;
+  static constexpr int epi_off = b_off + STAGES * B_STAGE_BYTES;
+  static constexpr int bar_off = epi_off + EPI_BYTES;
+  static constexpr int bar_bytes = (2 * STAGES + 4) * 8 + 16;
+  static constexpr int total = bar_off + bar_bytes;
+  static constexpr int alloc = total + 1024;  // runtime 1024-B alignment slack
+};
+static_assert(SmemLayout::alloc <= 232448, "smem budget");
+
+// Slab layout: for chunk c (32 cols) and float4 column-group j (0..7), the 128
+// rows are contiguous, so a warp's 32 lanes move 512 contiguous bytes per access.
+__device__ __forceinline__ float4* slab_ptr(float* slab, int c, int j, int row) {
+  return reinterpret_cast<float4*>(slab) + ((c * 8 + j) * BM + row);
+}
+
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    sk_gemm_f16_1sm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    const __grid_constant__ CUtensorMap tmC, const KernelParams P) {
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 1000)
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sA = smem + SmemLayout::a_off;
+  uint8_t* sB = smem + SmemLayout::b_off;
+  float* sEpi = reinterpret_cast<float*>(smem + SmemLayout::epi_off);
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + SmemLayout::bar_off);
+  uint64_t* empty_bar = full_bar + STAGES;
+  uint64_t* tfull_bar = empty_bar + STAGES;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const uint32_t warp = threadIdx.x / 32;
+  const uint32_t lane = threadIdx.x % 32;
+  const Schedule& s = P.s;
+  const int64_t cta = blockIdx.x;
+
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&tmA);
+    ptx::prefetch_tmap(&tmB);
+    ptx::prefetch_tmap(&tmC);
+    for (int i = 0; i < STAGES; ++i) {
+      ptx::mbar_init(&full_bar[i], 1);
+      ptx::mbar_init(&empty_bar[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(&tfull_bar[i], 1);
+      ptx::mbar_init(&tempty_bar[i], EPI_WARPS);
+    }
+    ptx::fence_barrier_init();
+  }
+  if (warp == 1) ptx::tmem_alloc<1>(tmem_base_smem, TMEM_COLS);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_base_smem;
+
+  if (warp == 0) {
+    // ===================== TMA producer =====================
+    if (lane == 0) {
+      const uint64_t pol = ptx::policy_evict_last();
+      uint32_t stage = 0, phase = 0;
+      for_each_segment(s, cta, P.num_ctas, [&](int64_t, int64_t tile, int64_t lb, int64_t le) {
+        const int32_t m0 = static_cast<int32_t>((tile / s.tiles_n) * BM);
+        const int32_t n0 = static_cast<int32_t>((tile % s.tiles_n) * BN);
+        for (int64_t kb = lb; kb < le; ++kb) {
+          ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
+          ptx::mbar_expect_tx(&full_bar[stage], A_STAGE_BYTES + B_STAGE_BYTES);
+          const int32_t k0 = static_cast<int32_t>(kb * BK);
+          ptx::tma_load_2d(sA + stage * A_STAGE_BYTES, &tmA, &full_bar[stage], k0, m0, pol);
+#pragma unroll
+          for (int i = 0; i < BN / 64; ++i)
+            ptx::tma_load_2d(sB + stage * B_STAGE_BYTES + i * B_BOX_BYTES, &tmB, &full_bar[stage],
+                             n0 + 64 * i, k0, pol);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      });
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ===================== tcgen05.mma issuer =====================
+    if (lane == 0) {
+      uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
+      for_each_segment(s, cta, P.num_ctas, [&](int64_t, int64_t, int64_t lb, int64_t le) {
+        ptx::mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int64_t kb = lb; kb < le; ++kb) {
+          ptx::mbar_wait(&full_bar[stage], phase);
+          ptx::tc_fence_after();
+          const uint32_t a0 = ptx::smem_u32(sA + stage * A_STAGE_BYTES);
+          const uint32_t b0 = ptx::smem_u32(sB + stage * B_STAGE_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < BK / UMMA_K; ++kk) {
+            // A: K-major SW128, +32 B per 16-element k step; SBO = 8 rows x 128 B.
+            const uint64_t ad = ptx::make_sdesc_sw128(a0 + kk * 32, 16, 1024);
+            // B: MN-major SW128, +16 k-rows x 128 B per k step; LBO = next 64-col box,
+            // SBO = 8 k-rows x 128 B.
+            const uint64_t bd = ptx::make_sdesc_sw128(b0 + kk * 2048, B_BOX_BYTES, 1024);
+            ptx::umma_f16<1>(d_tmem, ad, bd, P.idesc, (kb > lb || kk > 0) ? 1u : 0u);
+          }
+          ptx::umma_commit(&empty_bar[stage]);  // frees the smem slot when these MMAs finish
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        ptx::umma_commit(&tfull_bar[acc]);  // accumulator ready for the epilogue
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      });
+    }
+    __syncwarp();
+  } else {
+    // ===================== epilogue =====================
+    const uint32_t q = warp % 4;  // TMEM lane quarter this warp may access
+    const int row = static_cast<int>(q * 32 + lane);
+    const bool leader = (threadIdx.x == 64);
+    float* stage_buf = sEpi + (warp - 2) * 2 * (EPI_BUF_BYTES / 4);
+    float* partials = static_cast<float*>(P.partials);
+    uint32_t acc = 0, acc_phase = 0, nstores = 0;
+    for_each_segment(s, cta, P.num_ctas, [&](int64_t u, int64_t tile, int64_t lb, int64_t le) {
+      ptx::mbar_wait(&tfull_bar[acc], acc_phase);
+      ptx::tc_fence_after();
+      const uint32_t tsrc = tmem_base + acc * BN + ((q * 32) << 16);
+      const int32_t m0 = static_cast<int32_t>((tile / s.tiles_n) * BM);
+      const int32_t n0 = static_cast<int32_t>((tile % s.tiles_n) * BN);
+      const bool partial = lb != 0;  // not the tile starter (executor.hpp:160)
+      int64_t owner = u, last = u;
+      if (!partial && le < s.ipt) s.peers(tile, &owner, &last);
+      const int npeer = static_cast<int>(last - u);
+      if (npeer > 0) {
+        if (lane == 0)
+          for (int p = 1; p <= npeer; ++p) wait_flag(P, P.flags + s.slab_of(u + p));
+        __syncwarp();
+      }
+      float* my_slab = partial ? partials + s.slab_of(u) * static_cast<int64_t>(SLAB_ELEMS) : nullptr;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        float v[32];
+        ptx::tmem_ld32(tsrc + c * 32, v);
+        if (partial) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            ptx::st_cg_f4(slab_ptr(my_slab, c, j, row),
+                          make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
+        } else {
+          // Owner fold: own accumulator, then peers in ascending id (executor.hpp:165-172).
+#pragma unroll 1
+          for (int p = 1; p <= npeer; ++p) {
+            float* ps = partials + s.slab_of(u + p) * static_cast<int64_t>(SLAB_ELEMS);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const float4 w = ptx::ld_cg_f4(slab_ptr(ps, c, j, row));
+              v[4 * j] += w.x;
+              v[4 * j + 1] += w.y;
+              v[4 * j + 2] += w.z;
+              v[4 * j + 3] += w.w;
+            }
+          }
+          // Stage through swizzled smem (16-B chunk j of row r at j ^ (r % 8)), TMA store.
+          float* buf = stage_buf + (nstores & 1) * (EPI_BUF_BYTES / 4);
+          if (nstores >= 2) {
+            if (lane == 0) ptx::tma_store_wait_read<1>();
+            __syncwarp();
+          }
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int jj = j ^ static_cast<int>(lane & 7);
+            *reinterpret_cast<float4*>(buf + lane * 32 + jj * 4) =
+                make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          }
+          ptx::fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            ptx::tma_store_2d(&tmC, buf, n0 + c * 32, m0 + static_cast<int32_t>(q * 32));
+            ptx::tma_store_commit();
+          }
+          ++nstores;
+        }
+      }
+      // Accumulator drained: hand the TMEM buffer back to the MMA warp.
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&tempty_bar[acc]);
+      if (partial) {
+        __threadfence();
+        ptx::named_bar_sync(1, 32 * EPI_WARPS);
+        if (leader) {
+          signal_flag(P, P.flags + s.slab_of(u));
+          if (P.trace) atomicAdd(P.trace + 4 * s.total_tiles + u, 1);
+        }
+      } else {
+        if (npeer > 0) {
+          ptx::named_bar_sync(1, 32 * EPI_WARPS);
+          if (leader)  // every epilogue warp has read the slabs: re-arm the flags
+            for (int p = 1; p <= npeer; ++p) ptx::st_relaxed(P.flags + s.slab_of(u + p), 0);
+        }
+        if (leader && P.trace) {
+          int* t = P.trace + 4 * tile;
+          t[0] = static_cast<int>(owner);
+          t[1] = static_cast<int>(last);
+          t[2] = static_cast<int>(u);
+          t[3] = npeer;
+        }
+      }
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    });
+    if (lane == 0) ptx::tma_store_wait_all<0>();
+    __syncwarp();
+  }
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  if (warp == 1) ptx::tmem_dealloc<1>(tmem_base, TMEM_COLS);
+#endif
+}
+
+}  // namespace f16
+
+// tcgen05 instruction descriptor, kind::f16:
+//   [4,6) D format (1 = F32)  [7,10) A format  [10,13) B format (0 = F16, 1 = BF16)
+//   [15] A major (0 = K)  [16] B major (1 = MN)  [17,23) N >> 3  [24,29) M >> 4
+uint32_t make_idesc_f16(bool bf16, int M, int N) {
+  const uint32_t ab = bf16 ? 1u : 0u;
+  return (1u << 4) | (ab << 7) | (ab << 10) | (0u << 15) | (1u << 16) |
+         (static_cast<uint32_t>(N >> 3) << 17) | (static_cast<uint32_t>(M >> 4) << 24);
+}
+
+int f16_smem_bytes() { return f16::SmemLayout::alloc; }
+int f16_num_threads() { return f16::NUM_THREADS; }
+size_t f16_slab_bytes() { return sizeof(float) * f16::SLAB_ELEMS; }
+const void* f16_kernel_1sm() { return reinterpret_cast<const void*>(&f16::sk_gemm_f16_1sm); }
+
+cudaError_t launch_f16_1sm(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
+                           const KernelParams& p, int grid, cudaStream_t stream) {
+  static bool attr_set = false;  // per process; guarded by the caller's device-init mutex
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(f16::sk_gemm_f16_1sm,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         f16::SmemLayout::alloc);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  f16::sk_gemm_f16_1sm<<<grid, f16::NUM_THREADS, f16::SmemLayout::alloc, stream>>>(a, b, c, p);
+  return cudaGetLastError();
+}
+
+}  // namespace skb200

@@ -1,0 +1,523 @@
+// skb200_api.cu -- host side of the C ABI declared in include/skb200.h.
+//
+// Schedules are computed in closed form (schedule.hpp); sk_gemm validates the
+// descriptor, builds the TMA tensor maps, sizes the persistent grid to the SM
+// count and launches the hand-written sm_100a kernels.  sk_execute is the
+// reference-facing drop-in of streamk::execute<T> (executor.hpp:130-207):
+// host buffers in, host C out.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/skb200.h"
+#include "schedule.hpp"
+#include "sk_kernel_common.cuh"
+
+namespace skb200 {
+// sk_gemm_f16.cu
+uint32_t make_idesc_f16(bool bf16, int M, int N);
+int f16_smem_bytes();
+size_t f16_slab_bytes();
+cudaError_t launch_f16_1sm(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
+                           const KernelParams& p, int grid, cudaStream_t stream);
+// sk_convert.cu
+cudaError_t launch_f32_to_16(const float* src, void* dst, int64_t rows, int64_t cols,
+                             int64_t ld_dst, bool bf16, cudaStream_t stream);
+}  // namespace skb200
+
+using namespace skb200;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+sk_status fail(sk_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return st;
+}
+
+sk_status cuda_fail(cudaError_t e, const char* where) {
+  return fail(SK_ECUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+#define SK_CUDA(call)                                  \
+  do {                                                 \
+    cudaError_t e_ = (call);                           \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
+  } while (0)
+
+// ---- per-device lazily initialised state --------------------------------
+struct DeviceInfo {
+  int sms = 0;
+  int cc_major = 0, cc_minor = 0;
+  bool ok = false;
+};
+std::mutex g_dev_mu;
+DeviceInfo g_dev[64];
+
+sk_status device_info(int dev, DeviceInfo* out) {
+  if (dev < 0 || dev >= 64) return fail(SK_EINVAL, "device ordinal %d", dev);
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  DeviceInfo& d = g_dev[dev];
+  if (!d.ok) {
+    SK_CUDA(cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev));
+    SK_CUDA(cudaDeviceGetAttribute(&d.cc_major, cudaDevAttrComputeCapabilityMajor, dev));
+    SK_CUDA(cudaDeviceGetAttribute(&d.cc_minor, cudaDevAttrComputeCapabilityMinor, dev));
+    d.ok = true;
+  }
+  *out = d;
+  return SK_OK;
+}
+
+// ---- TMA descriptors through the driver entry point (no -lcuda) ----------
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return static_cast<EncodeTiledFn>(nullptr);
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  return fn;
+}
+
+// 2-D row-major tensor: rows x cols elements with leading dimension ld.
+sk_status make_tmap(CUtensorMap* m, CUtensorMapDataType dt, size_t esize, const void* base,
+                    int64_t rows, int64_t cols, int64_t ld, uint32_t box_cols, uint32_t box_rows,
+                    CUtensorMapSwizzle swz) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return fail(SK_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * esize};
+  const cuuint32_t box[2] = {box_cols, box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(SK_ECUDA, "cuTensorMapEncodeTiled failed (%d)", int(r));
+  return SK_OK;
+}
+
+bool valid_strategy(int32_t s) { return s >= 0 && s <= 4; }
+
+sk_status init_schedule(const sk_problem* p, const sk_blocking* b, int32_t strategy,
+                        int64_t param, Schedule* s) {
+  if (!p || !b) return fail(SK_EINVAL, "null problem/blocking");
+  if (!valid_strategy(strategy)) return fail(SK_EINVAL, "unknown strategy %d", strategy);
+  if (s->init(p->m, p->n, p->k, b->blk_m, b->blk_n, b->blk_k, strategy, param) != 0) {
+    if (p->m < 1 || p->n < 1 || p->k < 1) return fail(SK_EINVAL, "GemmProblem extents must be >= 1");
+    if (b->blk_m < 1 || b->blk_n < 1 || b->blk_k < 1)
+      return fail(SK_EINVAL, "BlockingFactors must be >= 1");
+    return fail(SK_EINVAL, "strategy parameter must be >= 1");
+  }
+  return SK_OK;
+}
+
+size_t dtype_size(int32_t t) {
+  switch (t) {
+    case SK_INT64: return 8;
+    case SK_FLOAT32: return 4;
+    case SK_FLOAT64: return 8;
+    case SK_BFLOAT16: return 2;
+    case SK_FLOAT16: return 2;
+  }
+  return 0;
+}
+
+// Which kernel serves a descriptor.
+enum class Kernel { F16_1SM, F16_2SM, F64 };
+
+sk_status pick_kernel(const sk_gemm_desc* d, Kernel* k) {
+  if (d->ab_type == SK_BFLOAT16 || d->ab_type == SK_FLOAT16) {
+    if (d->variant == SK_VARIANT_AUTO || d->variant == SK_VARIANT_1SM) {
+      *k = Kernel::F16_1SM;
+      return SK_OK;
+    }
+    return fail(SK_EUNSUPPORTED, "2-SM variant not built yet");
+  }
+  return fail(SK_EUNSUPPORTED, "ab_type %d has no device kernel", d->ab_type);
+}
+
+sk_status kernel_blocking(Kernel k, sk_blocking* out) {
+  switch (k) {
+    case Kernel::F16_1SM: *out = {128, 256, 64}; return SK_OK;
+    case Kernel::F16_2SM: *out = {256, 256, 64}; return SK_OK;
+    case Kernel::F64: *out = {64, 64, 16}; return SK_OK;
+  }
+  return SK_EINVAL;
+}
+
+int kernel_ranks(Kernel k) { return k == Kernel::F16_2SM ? 2 : 1; }
+
+size_t kernel_slab_bytes(Kernel k) {
+  switch (k) {
+    case Kernel::F16_1SM: return f16_slab_bytes();
+    case Kernel::F16_2SM: return f16_slab_bytes();
+    case Kernel::F64: return 64 * 64 * sizeof(double);
+  }
+  return 0;
+}
+
+sk_status check_desc(const sk_gemm_desc* d, Kernel* kern, Schedule* s) {
+  if (!d) return fail(SK_EINVAL, "null descriptor");
+  sk_status st = init_schedule(&d->problem, &d->blocking, d->strategy, d->param, s);
+  if (st) return st;
+  st = pick_kernel(d, kern);
+  if (st) return st;
+  sk_blocking kb;
+  kernel_blocking(*kern, &kb);
+  if (d->blocking.blk_m != kb.blk_m || d->blocking.blk_n != kb.blk_n ||
+      d->blocking.blk_k != kb.blk_k)
+    return fail(SK_EUNSUPPORTED,
+                "blocking %lldx%lldx%lld differs from the kernel tile %lldx%lldx%lld",
+                (long long)d->blocking.blk_m, (long long)d->blocking.blk_n,
+                (long long)d->blocking.blk_k, (long long)kb.blk_m, (long long)kb.blk_n,
+                (long long)kb.blk_k);
+  // int32 device indexing guard (true for every BASELINE config).
+  if (s->total_iters >= (int64_t(1) << 31) || s->grid_size >= (int64_t(1) << 31) ||
+      d->problem.m >= (int64_t(1) << 31) || d->problem.n >= (int64_t(1) << 31) ||
+      d->problem.k >= (int64_t(1) << 31))
+    return fail(SK_EUNSUPPORTED, "problem too large for 32-bit tile coordinates");
+  return SK_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* sk_status_string(sk_status s) {
+  switch (s) {
+    case SK_OK: return "SK_OK";
+    case SK_EINVAL: return "SK_EINVAL: invalid argument";
+    case SK_EUNSUPPORTED: return "SK_EUNSUPPORTED: not supported by the device kernel";
+    case SK_ECUDA: return "SK_ECUDA: CUDA error";
+    case SK_EPROTOCOL: return "SK_EPROTOCOL: fixup protocol violation";
+    case SK_ERANGE: return "SK_ERANGE: index out of range";
+    case SK_ECAPACITY: return "SK_ECAPACITY: output buffer too small";
+  }
+  return "unknown sk_status";
+}
+
+const char* sk_last_error(void) { return g_last_error.c_str(); }
+int sk_abi_version(void) { return SKB200_ABI_VERSION; }
+
+sk_status sk_tile_grid(const sk_problem* p, const sk_blocking* b, sk_tile_grid_t* out) {
+  Schedule s;
+  sk_status st = init_schedule(p, b, SK_DATA_PARALLEL, 1, &s);
+  if (st) return st;
+  if (out) *out = {s.tiles_m, s.tiles_n, s.total_tiles, s.ipt, s.total_iters};
+  return SK_OK;
+}
+
+sk_status sk_iter_to_coords(const sk_tile_grid_t* g, int64_t i, int64_t* tile, int64_t* local) {
+  if (!g || g->iters_per_tile < 1) return fail(SK_EINVAL, "bad tile grid");
+  if (i < 0 || i >= g->total_iters) return fail(SK_ERANGE, "iteration index out of range");
+  if (tile) *tile = i / g->iters_per_tile;
+  if (local) *local = i % g->iters_per_tile;
+  return SK_OK;
+}
+
+sk_status sk_schedule(const sk_problem* p, const sk_blocking* b, sk_strategy strategy,
+                      int64_t param, int64_t* grid_size, int64_t* ranges, int64_t capacity) {
+  Schedule s;
+  sk_status st = init_schedule(p, b, strategy, param, &s);
+  if (st) return st;
+  if (grid_size) *grid_size = s.grid_size;
+  if (!ranges) return SK_OK;
+  if (capacity < s.grid_size) return fail(SK_ECAPACITY, "ranges capacity %lld < g %lld",
+                                          (long long)capacity, (long long)s.grid_size);
+  for (int64_t u = 0; u < s.grid_size; ++u) s.range(u, &ranges[2 * u], &ranges[2 * u + 1]);
+  return SK_OK;
+}
+
+sk_status sk_fixup_peers(const sk_problem* p, const sk_blocking* b, sk_strategy strategy,
+                         int64_t param, int64_t* offsets, int64_t* ids, int64_t capacity,
+                         int64_t* nnz) {
+  Schedule s;
+  sk_status st = init_schedule(p, b, strategy, param, &s);
+  if (st) return st;
+  if (!offsets) return fail(SK_EINVAL, "null offsets");
+  int64_t total = 0;
+  offsets[0] = 0;
+  for (int64_t t = 0; t < s.total_tiles; ++t) {
+    int64_t owner, last;
+    s.peers(t, &owner, &last);
+    total += last - owner + 1;
+    offsets[t + 1] = total;
+  }
+  if (nnz) *nnz = total;
+  if (!ids) return SK_OK;
+  if (capacity < total) return fail(SK_ECAPACITY, "ids capacity too small");
+  int64_t q = 0;
+  for (int64_t t = 0; t < s.total_tiles; ++t) {
+    int64_t owner, last;
+    s.peers(t, &owner, &last);
+    for (int64_t id = owner; id <= last; ++id) ids[q++] = id;
+  }
+  return SK_OK;
+}
+
+sk_status sk_quantization_efficiency(int64_t t, int64_t p, double* out) {
+  if (t < 1 || p < 1) return fail(SK_EINVAL, "quantization_efficiency: t, p >= 1");
+  if (out) *out = static_cast<double>(t) / static_cast<double>(ceil_div(t, p) * p);
+  return SK_OK;
+}
+
+sk_status sk_kernel_blocking(sk_dtype ab_type, sk_variant variant, sk_blocking* out) {
+  sk_gemm_desc d{};
+  d.ab_type = ab_type;
+  d.variant = variant;
+  Kernel k;
+  sk_status st = pick_kernel(&d, &k);
+  if (st) return st;
+  return kernel_blocking(k, out);
+}
+
+sk_status sk_workspace_size(const sk_gemm_desc* d, size_t* bytes) {
+  Kernel k;
+  Schedule s;
+  sk_status st = check_desc(d, &k, &s);
+  if (st) return st;
+  WorkspaceLayout L;
+  L.compute(s.num_slabs, kernel_ranks(k), kernel_slab_bytes(k));
+  if (bytes) *bytes = L.total;
+  return SK_OK;
+}
+
+sk_status sk_workspace_init(void* ws, size_t bytes, void* stream) {
+  if (!ws || bytes < 256) return fail(SK_EINVAL, "workspace too small");
+  // One memset after allocation; the kernel re-arms every flag it consumes.
+  SK_CUDA(cudaMemsetAsync(ws, 0, bytes, static_cast<cudaStream_t>(stream)));
+  return SK_OK;
+}
+
+sk_status sk_workspace_check(void* ws, void* stream) {
+  if (!ws) return fail(SK_EINVAL, "null workspace");
+  int err = 0;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  SK_CUDA(cudaMemcpyAsync(&err, ws, sizeof(int), cudaMemcpyDeviceToHost, st));
+  SK_CUDA(cudaStreamSynchronize(st));
+  if (err == 0) return SK_OK;
+  SK_CUDA(cudaMemsetAsync(ws, 0, sizeof(int), st));
+  if (err & kErrDoubleSignal) return fail(SK_EPROTOCOL, "execute: fixup flag signaled twice");
+  return fail(SK_EPROTOCOL, "fixup wait watchdog expired (err=0x%x)", err);
+}
+
+sk_status sk_trace_size(const sk_gemm_desc* d, int64_t* ints) {
+  Kernel k;
+  Schedule s;
+  sk_status st = check_desc(d, &k, &s);
+  if (st) return st;
+  if (ints) *ints = 4 * s.total_tiles + s.grid_size;
+  return SK_OK;
+}
+
+sk_status sk_gemm(const sk_gemm_desc* d, void* ws, size_t ws_bytes, void* stream) {
+  Kernel kern;
+  Schedule s;
+  sk_status st = check_desc(d, &kern, &s);
+  if (st) return st;
+  const size_t esz = dtype_size(d->ab_type);
+  const size_t csz = d->ab_type == SK_FLOAT64 ? 8 : 4;
+  if (!d->A || !d->B || !d->C) return fail(SK_EINVAL, "null matrix pointer");
+  if (d->lda < d->problem.k || d->ldb < d->problem.n || d->ldc < d->problem.n)
+    return fail(SK_EINVAL, "leading dimension smaller than the row length");
+  if ((reinterpret_cast<uintptr_t>(d->A) | reinterpret_cast<uintptr_t>(d->B) |
+       reinterpret_cast<uintptr_t>(d->C)) & 15)
+    return fail(SK_EUNSUPPORTED, "matrix base pointers must be 16-byte aligned");
+  if ((d->lda * esz) % 16 || (d->ldb * esz) % 16 || (d->ldc * csz) % 16)
+    return fail(SK_EUNSUPPORTED, "leading dimensions must be multiples of 16 bytes (TMA)");
+  WorkspaceLayout L;
+  L.compute(s.num_slabs, kernel_ranks(kern), kernel_slab_bytes(kern));
+  if (!ws || ws_bytes < L.total)
+    return fail(SK_EINVAL, "workspace of %zu bytes < required %zu", ws_bytes, L.total);
+
+  int dev = 0;
+  SK_CUDA(cudaGetDevice(&dev));
+  DeviceInfo info;
+  st = device_info(dev, &info);
+  if (st) return st;
+  if (info.cc_major != 10 || info.cc_minor != 0)
+    return fail(SK_EUNSUPPORTED, "device sm_%d%d: this build targets sm_100a only", info.cc_major,
+                info.cc_minor);
+  cudaStream_t strm = static_cast<cudaStream_t>(stream);
+
+  KernelParams P{};
+  P.s = s;
+  P.ranks = kernel_ranks(kern);
+  uint8_t* wsb = static_cast<uint8_t*>(ws);
+  P.err = reinterpret_cast<int*>(wsb);
+  P.flags = reinterpret_cast<int*>(wsb + L.flags_off);
+  P.partials = wsb + L.partials_off;
+  P.trace = d->trace;
+  P.watchdog_ns = 4000000000LL;
+  const int64_t units = std::max<int64_t>(s.grid_size, 1);
+  const int64_t cap = d->num_ctas > 0 ? d->num_ctas : info.sms / P.ranks;
+  P.num_ctas = std::min<int64_t>(units, std::min<int64_t>(cap, info.sms / P.ranks));
+
+  if (kern == Kernel::F16_1SM) {
+    const CUtensorMapDataType dt = d->ab_type == SK_BFLOAT16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                                             : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+    CUtensorMap ta, tb, tc;
+    st = make_tmap(&ta, dt, 2, d->A, d->problem.m, d->problem.k, d->lda, 64, 128,
+                   CU_TENSOR_MAP_SWIZZLE_128B);
+    if (st) return st;
+    st = make_tmap(&tb, dt, 2, d->B, d->problem.k, d->problem.n, d->ldb, 64, 64,
+                   CU_TENSOR_MAP_SWIZZLE_128B);
+    if (st) return st;
+    st = make_tmap(&tc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, d->C, d->problem.m, d->problem.n,
+                   d->ldc, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B);
+    if (st) return st;
+    P.idesc = make_idesc_f16(d->ab_type == SK_BFLOAT16, 128, 256);
+    cudaError_t e;
+    {
+      std::lock_guard<std::mutex> lk(g_dev_mu);
+      e = launch_f16_1sm(ta, tb, tc, P, static_cast<int>(P.num_ctas), strm);
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "sk_gemm_f16_1sm launch");
+    return SK_OK;
+  }
+  return fail(SK_EUNSUPPORTED, "kernel not available");
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// sk_execute: streamk::execute<T> with host buffers (executor.hpp:130-207).
+// ---------------------------------------------------------------------------
+namespace {
+
+struct ExecCache {
+  int device = -1;
+  cudaStream_t stream = nullptr;
+  void* buf[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // A, B, C, ws, staging
+  size_t cap[5] = {0, 0, 0, 0, 0};
+  size_t ws_valid = 0;  // bytes of ws known to be zeroed
+  ~ExecCache() { release(); }
+  void release() {
+    if (device >= 0) cudaSetDevice(device);
+    for (int i = 0; i < 5; ++i) {
+      if (buf[i]) cudaFree(buf[i]);
+      buf[i] = nullptr;
+      cap[i] = 0;
+    }
+    if (stream) cudaStreamDestroy(stream);
+    stream = nullptr;
+    device = -1;
+    ws_valid = 0;
+  }
+  sk_status ensure(int i, size_t bytes) {
+    if (cap[i] >= bytes) return SK_OK;
+    if (buf[i]) cudaFree(buf[i]);
+    buf[i] = nullptr;
+    cap[i] = 0;
+    SK_CUDA(cudaMalloc(&buf[i], bytes));
+    cap[i] = bytes;
+    if (i == 3) ws_valid = 0;
+    return SK_OK;
+  }
+};
+thread_local ExecCache g_exec;
+
+int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+}  // namespace
+
+extern "C" sk_status sk_execute(const sk_problem* p, const sk_blocking* b, sk_strategy strategy,
+                                int64_t param, sk_dtype host_type, sk_dtype compute_type,
+                                int32_t variant, const void* A, const void* B, void* C,
+                                int32_t device) {
+  if (!p || !b || !A || !B || !C) return fail(SK_EINVAL, "null argument");
+  if (compute_type != SK_BFLOAT16 && compute_type != SK_FLOAT16 && compute_type != SK_FLOAT64)
+    return fail(SK_EUNSUPPORTED, "compute_type %d has no device kernel", compute_type);
+  const bool is16 = compute_type != SK_FLOAT64;
+  if (is16 && !(host_type == compute_type || host_type == SK_FLOAT32))
+    return fail(SK_EINVAL, "host_type must equal compute_type or be FLOAT32");
+  if (!is16 && host_type != SK_FLOAT64) return fail(SK_EINVAL, "FP64 compute needs FP64 host data");
+
+  int dev = device;
+  if (dev < 0) SK_CUDA(cudaGetDevice(&dev));
+  ExecCache& X = g_exec;
+  if (X.device != dev) {
+    X.release();
+    SK_CUDA(cudaSetDevice(dev));
+    SK_CUDA(cudaStreamCreateWithFlags(&X.stream, cudaStreamNonBlocking));
+    X.device = dev;
+  } else {
+    SK_CUDA(cudaSetDevice(dev));
+  }
+  const int64_t m = p->m, n = p->n, k = p->k;
+  if (m < 1 || n < 1 || k < 1) return fail(SK_EINVAL, "GemmProblem extents must be >= 1");
+  const size_t esz = dtype_size(compute_type), csz = is16 ? 4 : 8;
+  // Pitched device copies: ld rounded up to 16 bytes for TMA.
+  const int64_t lda = round_up(k, 16 / static_cast<int64_t>(esz));
+  const int64_t ldb = round_up(n, 16 / static_cast<int64_t>(esz));
+  const int64_t ldc = round_up(n, 16 / static_cast<int64_t>(csz));
+
+  sk_gemm_desc d{};
+  d.problem = *p;
+  d.blocking = *b;
+  d.strategy = strategy;
+  d.param = param;
+  d.ab_type = compute_type;
+  d.variant = variant;
+  d.lda = lda;
+  d.ldb = ldb;
+  d.ldc = ldc;
+  size_t ws_bytes = 0;
+  sk_status st = sk_workspace_size(&d, &ws_bytes);
+  if (st) return st;
+
+  st = X.ensure(0, static_cast<size_t>(m * lda) * esz);
+  if (!st) st = X.ensure(1, static_cast<size_t>(k * ldb) * esz);
+  if (!st) st = X.ensure(2, static_cast<size_t>(m * ldc) * csz);
+  if (!st) st = X.ensure(3, ws_bytes);
+  if (st) return st;
+  cudaStream_t s = X.stream;
+  if (X.ws_valid < ws_bytes) {
+    SK_CUDA(cudaMemsetAsync(X.buf[3], 0, ws_bytes, s));
+    X.ws_valid = ws_bytes;
+  }
+  if (host_type == SK_FLOAT32 && is16) {
+    // H2D fp32, round-to-nearest-even into the pitched 16-bit operand buffers.
+    st = X.ensure(4, static_cast<size_t>(std::max(m * k, k * n)) * 4);
+    if (st) return st;
+    float* stg = static_cast<float*>(X.buf[4]);
+    SK_CUDA(cudaMemcpyAsync(stg, A, sizeof(float) * m * k, cudaMemcpyHostToDevice, s));
+    SK_CUDA(launch_f32_to_16(stg, X.buf[0], m, k, lda, compute_type == SK_BFLOAT16, s));
+    SK_CUDA(cudaMemcpyAsync(stg, B, sizeof(float) * k * n, cudaMemcpyHostToDevice, s));
+    SK_CUDA(launch_f32_to_16(stg, X.buf[1], k, n, ldb, compute_type == SK_BFLOAT16, s));
+  } else {
+    SK_CUDA(cudaMemcpy2DAsync(X.buf[0], lda * esz, A, k * esz, k * esz, m, cudaMemcpyHostToDevice, s));
+    SK_CUDA(cudaMemcpy2DAsync(X.buf[1], ldb * esz, B, n * esz, n * esz, k, cudaMemcpyHostToDevice, s));
+  }
+  d.A = X.buf[0];
+  d.B = X.buf[1];
+  d.C = X.buf[2];
+  st = sk_gemm(&d, X.buf[3], ws_bytes, s);
+  if (st) return st;
+  SK_CUDA(cudaMemcpy2DAsync(C, n * csz, X.buf[2], ldc * csz, n * csz, m, cudaMemcpyDeviceToHost, s));
+  return sk_workspace_check(X.buf[3], s);
+}
+
+extern "C" void sk_execute_release(void) { g_exec.release(); }
