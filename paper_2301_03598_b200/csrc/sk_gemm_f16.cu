@@ -10,18 +10,22 @@
 //                                        release/acquire (sk_kernel_common.cuh)
 //   owner fold + StoreTile (:164-181) -> epilogue warps: TMEM -> regs (+ peer slabs in
 //                                        ascending id) -> swizzled smem -> TMA store
-//   worker loop (:187-193)            -> persistent grid, descending logical ids
+//   worker loop (:187-193)            -> persistent grid (sk_kernel_common.cuh)
+//
+// Two variants, one tile config each:
+//   CG = 1: 1-SM,  tile 128x256x64, tcgen05.mma.cta_group::1 M=128 N=256, grid = #SMs
+//   CG = 2: 2-SM,  tile 256x256x64, tcgen05.mma.cta_group::2 M=256 N=256 on a CTA
+//           pair (cluster of 2), grid = #SMs/2 pairs.  Each CTA of the pair loads
+//           its own 128 rows of A and its own 128 columns of B; the leader issues
+//           the MMA for both and every CTA drains its own 128 TMEM lanes.
 //
 // Warp roles (192 threads, 1 CTA per SM):
 //   warp 0      TMA producer (one lane)
-//   warp 1      TMEM allocator + tcgen05.mma issuer (one lane)
+//   warp 1      TMEM allocator + tcgen05.mma issuer (one lane; leader CTA only for CG=2)
 //   warps 2..5  epilogue; warp w drains TMEM lanes 32*(w%4) .. +31
-//
-// Tile config (one per precision): 1-SM 128x256x64.
-// The smem ring holds STAGES k-blocks: A 128x64 (K-major, 128B swizzle, 16 KB)
-// and B 64x256 as four 64x64 boxes (MN-major, 128B swizzle, 32 KB).
-// TMEM: two 256-column fp32 accumulators, so the epilogue of one segment
-// overlaps the mainloop of the next.
+// Smem ring: STAGES k-blocks of A (rows x 64, K-major, 128B swizzle) and B
+// (64 x cols as 64x64 boxes, MN-major, 128B swizzle).  TMEM: two 256-column
+// fp32 accumulators, so one segment's epilogue overlaps the next mainloop.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -33,97 +37,150 @@
 namespace skb200 {
 namespace f16 {
 
-constexpr int BM = 128;  // rows per CTA (per TMEM accumulator)
-constexpr int BN = 256;
+constexpr int ROWS = 128;  // rows per CTA (= TMEM lanes)
+constexpr int BN = 256;    // tile columns (MMA N)
 constexpr int BK = 64;
 constexpr int UMMA_K = 16;
-constexpr int STAGES = 4;
-constexpr int A_STAGE_BYTES = BM * BK * 2;           // 16 KB
-constexpr int B_BOX_BYTES = 64 * BK * 2;             // 8 KB: 64 k-rows x 64 n
-constexpr int B_STAGE_BYTES = BN * BK * 2;           // 32 KB
 constexpr int EPI_WARPS = 4;
-constexpr int EPI_BUF_BYTES = 32 * 32 * 4;           // 32 rows x 32 fp32 = 4 KB
-constexpr int EPI_BYTES = EPI_WARPS * 2 * EPI_BUF_BYTES;  // 32 KB
-constexpr int NUM_THREADS = 64 + 32 * EPI_WARPS;     // 192
-constexpr int TMEM_COLS = 512;                       // 2 x 256-col accumulators
-constexpr int SLAB_ELEMS = BM * BN;                  // fp32 partial per CTA rank
+constexpr int EPI_BUF_BYTES = 32 * 32 * 4;  // 32 rows x 32 fp32 = 4 KB
+constexpr int EPI_BYTES = EPI_WARPS * 2 * EPI_BUF_BYTES;
+constexpr int NUM_THREADS = 64 + 32 * EPI_WARPS;  // 192
+constexpr int TMEM_COLS = 512;                    // 2 x 256-col accumulators
+constexpr int SLAB_ELEMS = ROWS * BN;             // fp32 partial per CTA rank
+constexpr int B_BOX_BYTES = 64 * BK * 2;          // 64 k-rows x 64 cols
 
-struct SmemLayout {
+template <int CG>
+struct Cfg {
+  static constexpr int B_COLS = BN / CG;                    // B columns held per CTA
+  static constexpr int A_STAGE = ROWS * BK * 2;             // 16 KB
+  static constexpr int B_STAGE = B_COLS * BK * 2;           // 32 KB (1-SM) / 16 KB (2-SM)
+  static constexpr int STAGE = A_STAGE + B_STAGE;
+  static constexpr int STAGES = CG == 1 ? 4 : 6;
   static constexpr int a_off = 0;
-  static constexpr int b_off = a_off + STAGES * A_STAGE_BYTES;
-  static constexpr int epi_off = b_off + STAGES * B_STAGE_BYTES;
+  static constexpr int b_off = a_off + STAGES * A_STAGE;
+  static constexpr int epi_off = b_off + STAGES * B_STAGE;
   static constexpr int bar_off = epi_off + EPI_BYTES;
   static constexpr int bar_bytes = (2 * STAGES + 4) * 8 + 16;
-  static constexpr int total = bar_off + bar_bytes;
-  static constexpr int alloc = total + 1024;  // runtime 1024-B alignment slack
+  static constexpr int alloc = bar_off + bar_bytes + 1024;  // + runtime 1 KB alignment
+  static_assert(alloc <= 232448, "smem budget");
 };
-static_assert(SmemLayout::alloc <= 232448, "smem budget");
 
 // Slab layout: for chunk c (32 cols) and float4 column-group j (0..7), the 128
 // rows are contiguous, so a warp's 32 lanes move 512 contiguous bytes per access.
 __device__ __forceinline__ float4* slab_ptr(float* slab, int c, int j, int row) {
-  return reinterpret_cast<float4*>(slab) + ((c * 8 + j) * BM + row);
+  return reinterpret_cast<float4*>(slab) + ((c * 8 + j) * ROWS + row);
 }
 
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_id_x() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;"
+               ::: "memory");
+}
+// shared::cluster address of `p`'s twin in CTA `rank` of this cluster.
+__device__ __forceinline__ uint32_t mapa(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(ptx::smem_u32(p)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void tma_load_2d_to_leader(void* dst, const CUtensorMap* m,
+                                                      uint32_t bar_cluster_addr, int32_t c0,
+                                                      int32_t c1, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(ptx::smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(bar_cluster_addr), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t bar_cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster_addr)
+               : "memory");
+}
+
+template <int CG>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
-    sk_gemm_f16_1sm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                    const __grid_constant__ CUtensorMap tmC, const KernelParams P) {
+    sk_gemm_f16(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                const __grid_constant__ CUtensorMap tmC, const KernelParams P) {
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 1000)
+  using K = Cfg<CG>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  uint8_t* sA = smem + SmemLayout::a_off;
-  uint8_t* sB = smem + SmemLayout::b_off;
-  float* sEpi = reinterpret_cast<float*>(smem + SmemLayout::epi_off);
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + SmemLayout::bar_off);
-  uint64_t* empty_bar = full_bar + STAGES;
-  uint64_t* tfull_bar = empty_bar + STAGES;
+  uint8_t* sA = smem + K::a_off;
+  uint8_t* sB = smem + K::b_off;
+  float* sEpi = reinterpret_cast<float*>(smem + K::epi_off);
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + K::bar_off);
+  uint64_t* empty_bar = full_bar + K::STAGES;
+  uint64_t* tfull_bar = empty_bar + K::STAGES;
   uint64_t* tempty_bar = tfull_bar + 2;
   uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(tempty_bar + 2);
 
   const uint32_t warp = threadIdx.x / 32;
   const uint32_t lane = threadIdx.x % 32;
   const Schedule& s = P.s;
-  const int64_t cta = blockIdx.x;
+  const uint32_t rank = CG == 2 ? cluster_rank() : 0;
+  const bool leader_cta = rank == 0;
+  const int64_t cta = CG == 2 ? static_cast<int64_t>(cluster_id_x()) : static_cast<int64_t>(blockIdx.x);
 
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&tmA);
     ptx::prefetch_tmap(&tmB);
     ptx::prefetch_tmap(&tmC);
-    for (int i = 0; i < STAGES; ++i) {
+    for (int i = 0; i < K::STAGES; ++i) {
       ptx::mbar_init(&full_bar[i], 1);
       ptx::mbar_init(&empty_bar[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&tfull_bar[i], 1);
-      ptx::mbar_init(&tempty_bar[i], EPI_WARPS);
+      ptx::mbar_init(&tempty_bar[i], EPI_WARPS * CG);
     }
     ptx::fence_barrier_init();
   }
-  if (warp == 1) ptx::tmem_alloc<1>(tmem_base_smem, TMEM_COLS);
+  if (warp == 1) ptx::tmem_alloc<CG>(tmem_base_smem, TMEM_COLS);
   ptx::tc_fence_before();
   __syncthreads();
+  if constexpr (CG == 2) cluster_sync();  // peer barriers initialised before any remote use
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_base_smem;
 
   if (warp == 0) {
-    // ===================== TMA producer =====================
+    // ===================== TMA producer (every CTA of the pair) =====================
     if (lane == 0) {
       const uint64_t pol = ptx::policy_evict_last();
       uint32_t stage = 0, phase = 0;
-      for_each_segment(s, cta, P.num_ctas, [&](int64_t, int64_t tile, int64_t lb, int64_t le) {
-        const int32_t m0 = static_cast<int32_t>((tile / s.tiles_n) * BM);
-        const int32_t n0 = static_cast<int32_t>((tile % s.tiles_n) * BN);
+      for_each_segment(s, cta, P.num_ctas, P.raster_rows,
+                       [&](int64_t, int64_t tile, int64_t lb, int64_t le) {
+        const int32_t m0 = static_cast<int32_t>((tile / s.tiles_n) * (ROWS * CG) + rank * ROWS);
+        const int32_t n0 = static_cast<int32_t>((tile % s.tiles_n) * BN + rank * K::B_COLS);
         for (int64_t kb = lb; kb < le; ++kb) {
           ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
-          ptx::mbar_expect_tx(&full_bar[stage], A_STAGE_BYTES + B_STAGE_BYTES);
           const int32_t k0 = static_cast<int32_t>(kb * BK);
-          ptx::tma_load_2d(sA + stage * A_STAGE_BYTES, &tmA, &full_bar[stage], k0, m0, pol);
+          uint8_t* a_dst = sA + stage * K::A_STAGE;
+          uint8_t* b_dst = sB + stage * K::B_STAGE;
+          if constexpr (CG == 1) {
+            ptx::mbar_expect_tx(&full_bar[stage], K::STAGE);
+            ptx::tma_load_2d(a_dst, &tmA, &full_bar[stage], k0, m0, pol);
 #pragma unroll
-          for (int i = 0; i < BN / 64; ++i)
-            ptx::tma_load_2d(sB + stage * B_STAGE_BYTES + i * B_BOX_BYTES, &tmB, &full_bar[stage],
-                             n0 + 64 * i, k0, pol);
-          if (++stage == STAGES) {
+            for (int i = 0; i < K::B_COLS / 64; ++i)
+              ptx::tma_load_2d(b_dst + i * B_BOX_BYTES, &tmB, &full_bar[stage], n0 + 64 * i, k0, pol);
+          } else {
+            // Both CTAs' bytes land on the leader's full barrier; only the leader arrives.
+            if (leader_cta) ptx::mbar_expect_tx(&full_bar[stage], 2 * K::STAGE);
+            const uint32_t fb = mapa(&full_bar[stage], 0);
+            tma_load_2d_to_leader(a_dst, &tmA, fb, k0, m0, pol);
+#pragma unroll
+            for (int i = 0; i < K::B_COLS / 64; ++i)
+              tma_load_2d_to_leader(b_dst + i * B_BOX_BYTES, &tmB, fb, n0 + 64 * i, k0, pol);
+          }
+          if (++stage == K::STAGES) {
             stage = 0;
             phase ^= 1;
           }
@@ -133,17 +190,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     __syncwarp();
   } else if (warp == 1) {
     // ===================== tcgen05.mma issuer =====================
-    if (lane == 0) {
+    if (lane == 0 && leader_cta) {
       uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
-      for_each_segment(s, cta, P.num_ctas, [&](int64_t, int64_t, int64_t lb, int64_t le) {
+      for_each_segment(s, cta, P.num_ctas, P.raster_rows,
+                       [&](int64_t, int64_t, int64_t lb, int64_t le) {
         ptx::mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
         for (int64_t kb = lb; kb < le; ++kb) {
           ptx::mbar_wait(&full_bar[stage], phase);
           ptx::tc_fence_after();
-          const uint32_t a0 = ptx::smem_u32(sA + stage * A_STAGE_BYTES);
-          const uint32_t b0 = ptx::smem_u32(sB + stage * B_STAGE_BYTES);
+          const uint32_t a0 = ptx::smem_u32(sA + stage * K::A_STAGE);
+          const uint32_t b0 = ptx::smem_u32(sB + stage * K::B_STAGE);
 #pragma unroll
           for (int kk = 0; kk < BK / UMMA_K; ++kk) {
             // A: K-major SW128, +32 B per 16-element k step; SBO = 8 rows x 128 B.
@@ -151,15 +209,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             // B: MN-major SW128, +16 k-rows x 128 B per k step; LBO = next 64-col box,
             // SBO = 8 k-rows x 128 B.
             const uint64_t bd = ptx::make_sdesc_sw128(b0 + kk * 2048, B_BOX_BYTES, 1024);
-            ptx::umma_f16<1>(d_tmem, ad, bd, P.idesc, (kb > lb || kk > 0) ? 1u : 0u);
+            ptx::umma_f16<CG>(d_tmem, ad, bd, P.idesc, (kb > lb || kk > 0) ? 1u : 0u);
           }
-          ptx::umma_commit(&empty_bar[stage]);  // frees the smem slot when these MMAs finish
-          if (++stage == STAGES) {
+          // Free the smem slot(s) once these MMAs have read them.
+          if constexpr (CG == 1) ptx::umma_commit(&empty_bar[stage]);
+          else ptx::umma_commit_mc(&empty_bar[stage], 0x3);
+          if (++stage == K::STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        ptx::umma_commit(&tfull_bar[acc]);  // accumulator ready for the epilogue
+        // Accumulator ready for the epilogue warps (of both CTAs for CG = 2).
+        if constexpr (CG == 1) ptx::umma_commit(&tfull_bar[acc]);
+        else ptx::umma_commit_mc(&tfull_bar[acc], 0x3);
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
       });
@@ -173,11 +235,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     float* stage_buf = sEpi + (warp - 2) * 2 * (EPI_BUF_BYTES / 4);
     float* partials = static_cast<float*>(P.partials);
     uint32_t acc = 0, acc_phase = 0, nstores = 0;
-    for_each_segment(s, cta, P.num_ctas, [&](int64_t u, int64_t tile, int64_t lb, int64_t le) {
+    // flag / slab index of a (unit, rank): each CTA of a pair runs its own protocol
+    auto fidx = [&](int64_t u) { return s.slab_of(u) * CG + rank; };
+    for_each_segment(s, cta, P.num_ctas, P.raster_rows,
+                     [&](int64_t u, int64_t tile, int64_t lb, int64_t le) {
       ptx::mbar_wait(&tfull_bar[acc], acc_phase);
       ptx::tc_fence_after();
       const uint32_t tsrc = tmem_base + acc * BN + ((q * 32) << 16);
-      const int32_t m0 = static_cast<int32_t>((tile / s.tiles_n) * BM);
+      const int32_t m0 = static_cast<int32_t>((tile / s.tiles_n) * (ROWS * CG) + rank * ROWS);
       const int32_t n0 = static_cast<int32_t>((tile % s.tiles_n) * BN);
       const bool partial = lb != 0;  // not the tile starter (executor.hpp:160)
       int64_t owner = u, last = u;
@@ -185,10 +250,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const int npeer = static_cast<int>(last - u);
       if (npeer > 0) {
         if (lane == 0)
-          for (int p = 1; p <= npeer; ++p) wait_flag(P, P.flags + s.slab_of(u + p));
+          for (int p = 1; p <= npeer; ++p) wait_flag(P, P.flags + fidx(u + p));
         __syncwarp();
       }
-      float* my_slab = partial ? partials + s.slab_of(u) * static_cast<int64_t>(SLAB_ELEMS) : nullptr;
+      float* my_slab = partial ? partials + fidx(u) * static_cast<int64_t>(SLAB_ELEMS) : nullptr;
 #pragma unroll 1
       for (int c = 0; c < BN / 32; ++c) {
         float v[32];
@@ -202,7 +267,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           // Owner fold: own accumulator, then peers in ascending id (executor.hpp:165-172).
 #pragma unroll 1
           for (int p = 1; p <= npeer; ++p) {
-            float* ps = partials + s.slab_of(u + p) * static_cast<int64_t>(SLAB_ELEMS);
+            float* ps = partials + fidx(u + p) * static_cast<int64_t>(SLAB_ELEMS);
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
               const float4 w = ptx::ld_cg_f4(slab_ptr(ps, c, j, row));
@@ -233,24 +298,27 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           ++nstores;
         }
       }
-      // Accumulator drained: hand the TMEM buffer back to the MMA warp.
+      // Accumulator drained: hand the TMEM buffer back to the (leader's) MMA warp.
       ptx::tc_fence_before();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&tempty_bar[acc]);
+      if (lane == 0) {
+        if constexpr (CG == 1) ptx::mbar_arrive(&tempty_bar[acc]);
+        else mbar_arrive_remote(mapa(&tempty_bar[acc], 0));
+      }
       if (partial) {
         __threadfence();
         ptx::named_bar_sync(1, 32 * EPI_WARPS);
         if (leader) {
-          signal_flag(P, P.flags + s.slab_of(u));
-          if (P.trace) atomicAdd(P.trace + 4 * s.total_tiles + u, 1);
+          signal_flag(P, P.flags + fidx(u));
+          if (P.trace && rank == 0) atomicAdd(P.trace + 4 * s.total_tiles + u, 1);
         }
       } else {
         if (npeer > 0) {
           ptx::named_bar_sync(1, 32 * EPI_WARPS);
           if (leader)  // every epilogue warp has read the slabs: re-arm the flags
-            for (int p = 1; p <= npeer; ++p) ptx::st_relaxed(P.flags + s.slab_of(u + p), 0);
+            for (int p = 1; p <= npeer; ++p) ptx::st_relaxed(P.flags + fidx(u + p), 0);
         }
-        if (leader && P.trace) {
+        if (leader && P.trace && rank == 0) {
           int* t = P.trace + 4 * tile;
           t[0] = static_cast<int>(owner);
           t[1] = static_cast<int>(last);
@@ -267,8 +335,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   ptx::tc_fence_before();
   __syncthreads();
+  if constexpr (CG == 2) cluster_sync();  // the leader's MMAs touch the peer's smem/TMEM
   ptx::tc_fence_after();
-  if (warp == 1) ptx::tmem_dealloc<1>(tmem_base, TMEM_COLS);
+  if (warp == 1) ptx::tmem_dealloc<CG>(tmem_base, TMEM_COLS);
 #endif
 }
 
@@ -283,23 +352,41 @@ uint32_t make_idesc_f16(bool bf16, int M, int N) {
          (static_cast<uint32_t>(N >> 3) << 17) | (static_cast<uint32_t>(M >> 4) << 24);
 }
 
-int f16_smem_bytes() { return f16::SmemLayout::alloc; }
-int f16_num_threads() { return f16::NUM_THREADS; }
 size_t f16_slab_bytes() { return sizeof(float) * f16::SLAB_ELEMS; }
-const void* f16_kernel_1sm() { return reinterpret_cast<const void*>(&f16::sk_gemm_f16_1sm); }
 
-cudaError_t launch_f16_1sm(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
-                           const KernelParams& p, int grid, cudaStream_t stream) {
-  static bool attr_set = false;  // per process; guarded by the caller's device-init mutex
+template <int CG>
+static cudaError_t launch_cg(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
+                             const KernelParams& p, int pairs_or_ctas, cudaStream_t stream) {
+  static bool attr_set = false;  // guarded by the caller's device-init mutex
+  auto kern = f16::sk_gemm_f16<CG>;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(f16::sk_gemm_f16_1sm,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         f16::SmemLayout::alloc);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         f16::Cfg<CG>::alloc);
     if (e != cudaSuccess) return e;
+    if (CG == 2) {
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
+      if (e != cudaSuccess) return e;
+    }
     attr_set = true;
   }
-  f16::sk_gemm_f16_1sm<<<grid, f16::NUM_THREADS, f16::SmemLayout::alloc, stream>>>(a, b, c, p);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(pairs_or_ctas * CG));
+  cfg.blockDim = dim3(f16::NUM_THREADS);
+  cfg.dynamicSmemBytes = f16::Cfg<CG>::alloc;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, a, b, c, p);
+}
+
+cudaError_t launch_f16(int cg, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
+                       const KernelParams& p, int grid, cudaStream_t stream) {
+  return cg == 2 ? launch_cg<2>(a, b, c, p, grid, stream) : launch_cg<1>(a, b, c, p, grid, stream);
 }
 
 }  // namespace skb200

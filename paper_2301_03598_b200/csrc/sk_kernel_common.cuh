@@ -40,29 +40,73 @@ struct KernelParams {
   int* err;
   int* trace;
   int64_t watchdog_ns;
+  int64_t raster_rows;  // data-parallel tile-row group height (1 = row-major)
 };
 
-// The persistent schedule: physical CTA `cta` of `P` runs logical CTAs
-// g-1-cta, g-1-cta-P, ... (descending, like executor.hpp:187-193), and inside
-// each logical CTA its tile segments in ascending iteration order
-// (executor.hpp:149-185).  Every wait targets a strictly higher logical id and
-// every CTA's pending ids are lower than its current one, so with all P CTAs
-// co-resident the highest in-flight id never waits on unfinished work.
+// Data-parallel slot i -> tile, a bijection on [0, dp_tiles): whole tile rows
+// are visited in groups of `rows` rows, column-major inside a group, so one
+// wave of persistent CTAs covers a compact rows x (P / rows) block whose A and
+// B panels stay L2-resident; the trailing partial row is visited in order.
+// Only the temporal order changes: unit <-> range <-> tile stays the
+// reference's (decompose.cpp:42-46), so schedule parity is unaffected.
+__device__ __forceinline__ int64_t raster_tile(const Schedule& s, int64_t i, int64_t rows) {
+  const int64_t full_rows = s.dp_tiles / s.tiles_n;
+  if (rows <= 1 || i >= full_rows * s.tiles_n) return i;
+  const int64_t group = rows * s.tiles_n;
+  const int64_t gi = i / group, within = i - gi * group;
+  const int64_t h = imin(rows, full_rows - gi * rows);
+  const int64_t col = within / h, row = gi * rows + (within - col * h);
+  return row * s.tiles_n + col;
+}
+
+// The persistent schedule.  Dependencies only run from a tile's owner to
+// strictly higher ids inside the balanced (Stream-K) region or inside a
+// fixed-split tile; data-parallel units never wait and are never waited on.
+//   * data-parallel units: physical CTA `cta` of `P` takes slots cta, cta+P, ...
+//     of the rasterised order above;
+//   * balanced / fixed-split units: ids hi-1-cta, hi-1-cta-P, ... descending,
+//     like the reference's dispatch (executor.hpp:187-193).  Every CTA's pending
+//     ids are lower than its current one and every wait targets a higher id, so
+//     with all P CTAs co-resident the highest in-flight id never waits on
+//     unfinished work (executor.hpp:124-129).
+// The phases run in descending-id order of the reference (DP ids above the SK
+// ids for TwoTileSkDp, below for DpOneTileSk).  Inside a unit, segments run in
+// ascending iteration order (executor.hpp:149-185).  Producer, MMA and epilogue
+// roles all walk this same sequence.
+template <class F>
+__device__ __forceinline__ void run_unit(const Schedule& s, int64_t u, F& f) {
+  int64_t b, e;
+  s.range(u, &b, &e);
+  int64_t it = b;
+  while (it < e) {
+    const int64_t tile = it / s.ipt;
+    const int64_t tb = tile * s.ipt;
+    const int64_t lb = it - tb;
+    const int64_t le = imin(e, tb + s.ipt) - tb;
+    f(u, tile, lb, le);
+    it = tb + s.ipt;
+  }
+}
+
 template <class F>
 __device__ __forceinline__ void for_each_segment(const Schedule& s, int64_t cta, int64_t P,
-                                                 F&& f) {
-  for (int64_t u = s.grid_size - 1 - cta; u >= 0; u -= P) {
-    int64_t b, e;
-    s.range(u, &b, &e);
-    int64_t it = b;
-    while (it < e) {
-      const int64_t tile = it / s.ipt;
-      const int64_t tb = tile * s.ipt;
-      const int64_t lb = it - tb;
-      const int64_t le = imin(e, tb + s.ipt) - tb;
-      f(u, tile, lb, le);
-      it = tb + s.ipt;
-    }
+                                                 int64_t raster_rows, F&& f) {
+  auto dp_phase = [&] {
+    for (int64_t i = cta; i < s.dp_tiles; i += P) run_unit(s, s.dp_id0 + raster_tile(s, i, raster_rows), f);
+  };
+  auto desc_phase = [&](int64_t lo, int64_t hi) {
+    for (int64_t u = hi - 1 - cta; u >= lo; u -= P) run_unit(s, u, f);
+  };
+  if (s.strategy == kFixedSplit) {
+    desc_phase(0, s.grid_size);
+  } else if (s.bal.count == 0) {
+    dp_phase();
+  } else if (s.dp_id0 > s.bal.first_id) {  // TwoTileSkDp: DP ids above the SK ids
+    dp_phase();
+    desc_phase(s.bal.first_id, s.bal.first_id + s.bal.count);
+  } else {  // StreamK, DpOneTileSk: SK ids above the DP ids
+    desc_phase(s.bal.first_id, s.bal.first_id + s.bal.count);
+    dp_phase();
   }
 }
 

@@ -13,9 +13,11 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/skb200.h"
@@ -25,10 +27,9 @@
 namespace skb200 {
 // sk_gemm_f16.cu
 uint32_t make_idesc_f16(bool bf16, int M, int N);
-int f16_smem_bytes();
 size_t f16_slab_bytes();
-cudaError_t launch_f16_1sm(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
-                           const KernelParams& p, int grid, cudaStream_t stream);
+cudaError_t launch_f16(int cg, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
+                       const KernelParams& p, int grid, cudaStream_t stream);
 // sk_convert.cu
 cudaError_t launch_f32_to_16(const float* src, void* dst, int64_t rows, int64_t cols,
                              int64_t ld_dst, bool bf16, cudaStream_t stream);
@@ -118,6 +119,49 @@ sk_status make_tmap(CUtensorMap* m, CUtensorMapDataType dt, size_t esize, const 
   return SK_OK;
 }
 
+// ---- workspace hygiene ------------------------------------------------------
+// The kernels leave every flag they consume at zero, but the flag region's size
+// depends on the schedule, so a workspace reused across descriptors may have old
+// partial-slab bytes where the next launch keeps its flags.  Track, per
+// workspace, the hull of bytes that may hold slab data and clear a new launch's
+// flag region only when it overlaps that hull.
+struct Dirty {
+  size_t lo = 0, hi = 0;  // [lo, hi), empty when lo >= hi
+};
+std::mutex g_ws_mu;
+std::unordered_map<const void*, Dirty> g_ws_dirty;
+
+void ws_mark_clean(const void* ws) {
+  std::lock_guard<std::mutex> lk(g_ws_mu);
+  g_ws_dirty[ws] = Dirty{};
+}
+void ws_mark_all_dirty(const void* ws) {
+  std::lock_guard<std::mutex> lk(g_ws_mu);
+  g_ws_dirty[ws] = Dirty{0, ~size_t(0)};
+}
+// Returns true when [flags_off, flags_end) must be zeroed before this launch.
+bool ws_prepare(const void* ws, size_t flags_off, size_t flags_end, size_t slabs_end) {
+  std::lock_guard<std::mutex> lk(g_ws_mu);
+  auto it = g_ws_dirty.find(ws);
+  bool clear = false;
+  Dirty d = it == g_ws_dirty.end() ? Dirty{} : it->second;
+  if (d.lo < d.hi && d.lo < flags_end && flags_off < d.hi) {
+    clear = true;
+    if (d.lo < flags_end) d.lo = flags_end;
+  }
+  if (slabs_end > flags_end) {  // this launch writes slabs in [flags_end, slabs_end)
+    if (d.lo >= d.hi) {
+      d.lo = flags_end;
+      d.hi = slabs_end;
+    } else {
+      d.lo = std::min(d.lo, flags_end);
+      d.hi = std::max(d.hi, slabs_end);
+    }
+  }
+  g_ws_dirty[ws] = d;
+  return clear;
+}
+
 bool valid_strategy(int32_t s) { return s >= 0 && s <= 4; }
 
 sk_status init_schedule(const sk_problem* p, const sk_blocking* b, int32_t strategy,
@@ -153,7 +197,11 @@ sk_status pick_kernel(const sk_gemm_desc* d, Kernel* k) {
       *k = Kernel::F16_1SM;
       return SK_OK;
     }
-    return fail(SK_EUNSUPPORTED, "2-SM variant not built yet");
+    if (d->variant == SK_VARIANT_2SM) {
+      *k = Kernel::F16_2SM;
+      return SK_OK;
+    }
+    return fail(SK_EINVAL, "unknown variant %d", d->variant);
   }
   return fail(SK_EUNSUPPORTED, "ab_type %d has no device kernel", d->ab_type);
 }
@@ -308,6 +356,7 @@ sk_status sk_workspace_init(void* ws, size_t bytes, void* stream) {
   if (!ws || bytes < 256) return fail(SK_EINVAL, "workspace too small");
   // One memset after allocation; the kernel re-arms every flag it consumes.
   SK_CUDA(cudaMemsetAsync(ws, 0, bytes, static_cast<cudaStream_t>(stream)));
+  ws_mark_clean(ws);
   return SK_OK;
 }
 
@@ -319,6 +368,7 @@ sk_status sk_workspace_check(void* ws, void* stream) {
   SK_CUDA(cudaStreamSynchronize(st));
   if (err == 0) return SK_OK;
   SK_CUDA(cudaMemsetAsync(ws, 0, sizeof(int), st));
+  ws_mark_all_dirty(ws);  // flags may be left set after a protocol failure
   if (err & kErrDoubleSignal) return fail(SK_EPROTOCOL, "execute: fixup flag signaled twice");
   return fail(SK_EPROTOCOL, "fixup wait watchdog expired (err=0x%x)", err);
 }
@@ -361,6 +411,8 @@ sk_status sk_gemm(const sk_gemm_desc* d, void* ws, size_t ws_bytes, void* stream
     return fail(SK_EUNSUPPORTED, "device sm_%d%d: this build targets sm_100a only", info.cc_major,
                 info.cc_minor);
   cudaStream_t strm = static_cast<cudaStream_t>(stream);
+  if (ws_prepare(ws, L.flags_off, L.partials_off, L.total))
+    SK_CUDA(cudaMemsetAsync(static_cast<uint8_t*>(ws) + L.flags_off, 0, L.flag_bytes, strm));
 
   KernelParams P{};
   P.s = s;
@@ -371,11 +423,14 @@ sk_status sk_gemm(const sk_gemm_desc* d, void* ws, size_t ws_bytes, void* stream
   P.partials = wsb + L.partials_off;
   P.trace = d->trace;
   P.watchdog_ns = 4000000000LL;
+  P.raster_rows = 16;
+  if (const char* e = getenv("SKB200_RASTER_ROWS")) P.raster_rows = std::max(1, atoi(e));
   const int64_t units = std::max<int64_t>(s.grid_size, 1);
   const int64_t cap = d->num_ctas > 0 ? d->num_ctas : info.sms / P.ranks;
   P.num_ctas = std::min<int64_t>(units, std::min<int64_t>(cap, info.sms / P.ranks));
 
-  if (kern == Kernel::F16_1SM) {
+  if (kern == Kernel::F16_1SM || kern == Kernel::F16_2SM) {
+    const int cg = kern == Kernel::F16_2SM ? 2 : 1;
     const CUtensorMapDataType dt = d->ab_type == SK_BFLOAT16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
                                                              : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
     CUtensorMap ta, tb, tc;
@@ -388,13 +443,13 @@ sk_status sk_gemm(const sk_gemm_desc* d, void* ws, size_t ws_bytes, void* stream
     st = make_tmap(&tc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, d->C, d->problem.m, d->problem.n,
                    d->ldc, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B);
     if (st) return st;
-    P.idesc = make_idesc_f16(d->ab_type == SK_BFLOAT16, 128, 256);
+    P.idesc = make_idesc_f16(d->ab_type == SK_BFLOAT16, 128 * cg, 256);
     cudaError_t e;
     {
       std::lock_guard<std::mutex> lk(g_dev_mu);
-      e = launch_f16_1sm(ta, tb, tc, P, static_cast<int>(P.num_ctas), strm);
+      e = launch_f16(cg, ta, tb, tc, P, static_cast<int>(P.num_ctas), strm);
     }
-    if (e != cudaSuccess) return cuda_fail(e, "sk_gemm_f16_1sm launch");
+    if (e != cudaSuccess) return cuda_fail(e, cg == 2 ? "sk_gemm_f16<2> launch" : "sk_gemm_f16<1> launch");
     return SK_OK;
   }
   return fail(SK_EUNSUPPORTED, "kernel not available");
@@ -495,8 +550,9 @@ extern "C" sk_status sk_execute(const sk_problem* p, const sk_blocking* b, sk_st
   if (st) return st;
   cudaStream_t s = X.stream;
   if (X.ws_valid < ws_bytes) {
-    SK_CUDA(cudaMemsetAsync(X.buf[3], 0, ws_bytes, s));
-    X.ws_valid = ws_bytes;
+    st = sk_workspace_init(X.buf[3], X.cap[3], s);
+    if (st) return st;
+    X.ws_valid = X.cap[3];
   }
   if (host_type == SK_FLOAT32 && is16) {
     // H2D fp32, round-to-nearest-even into the pitched 16-bit operand buffers.

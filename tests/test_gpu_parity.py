@@ -1,0 +1,188 @@
+"""GPU parity: the sm_100a Stream-K kernels against the oracle.
+
+* Integer-valued operands (the reference's random_matrix<int64> band, exact in
+  bf16/fp16, products and partial sums exact in fp32 below 2^24): C must be
+  BIT-exact versus the oracle's int64 execute, for every decomposition.
+* Random uniform [-1, 1) operands rounded to bf16/fp16: within the reference's
+  own verify bound |c - ref| <= 8 * eps_fp32 * k * max(|ref|, 1)
+  (executor.hpp:217-239), eps_fp32 = 2^-23 (fp32 accumulate), ref = oracle
+  gemm_reference<float> on the same rounded values.
+* Ownership: the device-recorded owner / last peer of every tile equals the
+  reference's fixup_peers_of.
+"""
+import numpy as np
+import pytest
+
+import __graft_entry__
+
+pytestmark = pytest.mark.gpu
+
+NAMES = ["data_parallel", "fixed_split", "stream_k", "dp_one_tile_sk", "two_tile_sk_dp"]
+EPS32 = float(np.finfo(np.float32).eps)
+
+
+def strategies(sk, problem, blk, p=148):
+    yield sk.data_parallel(problem, blk)
+    yield sk.fixed_split(problem, blk, 3)
+    yield sk.stream_k(problem, blk, p)
+    yield sk.stream_k(problem, blk, 7)
+    yield sk.hybrid(problem, blk, p, sk.HybridVariant.DpOneTileSk)
+    yield sk.hybrid(problem, blk, p, sk.HybridVariant.TwoTileSkDp)
+    yield sk.hybrid(problem, blk, 5, sk.HybridVariant.TwoTileSkDp)
+
+
+def int_operands(port, m, n, k, seed, shift=0):
+    A = port.random_matrix(m, k, seed, "int64") >> shift
+    B = port.random_matrix(k, n, seed + 1, "int64") >> shift
+    return A, B
+
+
+def to_bf16_f32(x):
+    """Round float32 to the nearest bfloat16 (RNE), returned as float32."""
+    u = np.ascontiguousarray(x, np.float32).view(np.uint32)
+    r = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16) << 16
+    return r.astype(np.uint32).view(np.float32)
+
+
+def test_smoke():
+    __graft_entry__.smoke()
+
+
+@pytest.mark.parametrize("shape", [(128, 256, 64), (384, 768, 1000), (129, 257, 65),
+                                   (1000, 1000, 520), (256, 512, 4096), (640, 1280, 192)])
+def test_int_bit_exact_all_strategies_execute(sk, port, shape):
+    m, n, k = shape
+    blk = sk.kernel_blocking()
+    A, B = int_operands(port, m, n, k, 1234 + m)
+    want = port.execute("data_parallel", 1, A, B, blk.blk_m, blk.blk_n, blk.blk_k).astype(np.float32)
+    Af, Bf = A.astype(np.float32), B.astype(np.float32)
+    for a in strategies(sk, sk.GemmProblem(m, n, k), blk):
+        got = sk.execute(a, Af, Bf, compute=sk.DType.BFloat16)
+        assert np.array_equal(got, want), (sk.strategy_name(a.strategy), a.param)
+
+
+def test_int_bit_exact_fp16(sk, port):
+    m, n, k = 512, 768, 640
+    blk = sk.kernel_blocking(sk.DType.Float16)
+    A, B = int_operands(port, m, n, k, 77)
+    want = (A @ B).astype(np.float32)
+    for a in strategies(sk, sk.GemmProblem(m, n, k), blk):
+        got = sk.execute(a, A.astype(np.float16), B.astype(np.float16), compute=sk.DType.Float16)
+        assert np.array_equal(got, want), sk.strategy_name(a.strategy)
+
+
+def test_edge_schedules_bit_exact(sk, port):
+    """g > total_iters (empty units), one deep-k tile split 148 ways, the
+    pathological DpOneTileSk (150 tiles, p=148: 20 empty ranges, 64 peers)."""
+    blk = sk.kernel_blocking()
+    cases = [
+        (sk.GemmProblem(128, 256, 128), lambda p: sk.stream_k(p, blk, 148)),
+        (sk.GemmProblem(128, 256, 16384), lambda p: sk.stream_k(p, blk, 148)),
+        (sk.GemmProblem(128, 256, 16384), lambda p: sk.fixed_split(p, blk, 5)),
+        (sk.GemmProblem(1280, 3840, 1024), lambda p: sk.hybrid(p, blk, 148, sk.HybridVariant.DpOneTileSk)),
+        (sk.GemmProblem(1280, 3840, 1024), lambda p: sk.hybrid(p, blk, 148, sk.HybridVariant.TwoTileSkDp)),
+    ]
+    for problem, make in cases:
+        a = make(problem)
+        # values in [-8, 7]: |partial sums| <= 64 * 16384 < 2^24, exact in fp32
+        A, B = int_operands(port, problem.m, problem.n, problem.k, 99, shift=3)
+        want = (A.astype(np.float64) @ B.astype(np.float64)).astype(np.float32)  # exact
+        got = sk.execute(a, A.astype(np.float32), B.astype(np.float32))
+        assert np.array_equal(got, want), (problem, sk.strategy_name(a.strategy))
+
+
+def test_float_within_reference_bound(sk, port):
+    m, n, k = 768, 1024, 2000
+    blk = sk.kernel_blocking()
+    A = to_bf16_f32(port.random_matrix(m, k, 42, "float32"))
+    B = to_bf16_f32(port.random_matrix(k, n, 43, "float32"))
+    ref = port.gemm_reference(A, B, blk.blk_m, blk.blk_n, blk.blk_k)
+    import oracle
+
+    for a in strategies(sk, sk.GemmProblem(m, n, k), blk):
+        got = sk.execute(a, A, B)
+        ok, max_abs, max_rel = oracle.verify(got, ref, k, EPS32)
+        assert ok, (sk.strategy_name(a.strategy), max_abs, max_rel)
+
+
+def test_device_path_deterministic_and_self_cleaning(sk, torch_cuda):
+    torch = torch_cuda
+    m = n = 2048
+    k = 4096
+    blk = sk.kernel_blocking()
+    g = torch.Generator(device="cuda").manual_seed(0)
+    A = torch.rand(m, k, device="cuda", generator=g).mul_(2).sub_(1).to(torch.bfloat16)
+    B = torch.rand(k, n, device="cuda", generator=g).mul_(2).sub_(1).to(torch.bfloat16)
+    ref = A.double() @ B.double()
+    for a in (sk.stream_k(sk.GemmProblem(m, n, k), blk, 148),
+              sk.hybrid(sk.GemmProblem(m, n, k), blk, 148, sk.HybridVariant.DpOneTileSk)):
+        gemm = sk.Gemm(a)
+        outs = []
+        for _ in range(5):
+            C = torch.full((m, n), float("nan"), device="cuda")
+            gemm.run(A, B, C)
+            outs.append(C)
+        gemm.check()
+        for C in outs[1:]:
+            assert torch.equal(C, outs[0])  # fixed fold order: run-to-run identical
+        err = (outs[0].double() - ref).abs()
+        bound = 8 * EPS32 * k * ref.abs().clamp(min=1)
+        assert bool((err <= bound).all())
+        # flags re-armed by the owners: the whole flag region is zero again
+        flags = gemm.workspace[256:256 + 4 * 512].view(torch.int32)
+        assert int(flags.abs().sum()) == 0
+
+
+def test_trace_ownership_equals_fixup_peers_of(sk, torch_cuda):
+    torch = torch_cuda
+    blk = sk.kernel_blocking()
+    for problem, p in ((sk.GemmProblem(1024, 1024, 32768), 148), (sk.GemmProblem(1280, 3840, 512), 148),
+                       (sk.GemmProblem(2048, 2048, 1024), 37)):
+        for strat in (sk.Strategy.StreamK, sk.Strategy.FixedSplit, sk.Strategy.DpOneTileSk,
+                      sk.Strategy.TwoTileSkDp, sk.Strategy.DataParallel):
+            param = {sk.Strategy.FixedSplit: 3, sk.Strategy.DataParallel: 1}.get(strat, p)
+            a = sk._assignment(strat, problem, blk, param)
+            gemm = sk.Gemm(a, trace=True)
+            A = torch.zeros(problem.m, problem.k, dtype=torch.bfloat16, device="cuda")
+            B = torch.zeros(problem.k, problem.n, dtype=torch.bfloat16, device="cuda")
+            C = torch.empty(problem.m, problem.n, device="cuda")
+            gemm.run(A, B, C)
+            gemm.check()
+            t = gemm.trace.cpu().numpy()
+            T = a.grid.total_tiles
+            tiles = t[:4 * T].reshape(T, 4)
+            peers = sk.fixup_peers_of(a)
+            for x in range(T):
+                assert tiles[x, 0] == peers[x][0] and tiles[x, 1] == peers[x][-1], (strat, x)
+                assert tiles[x, 2] == peers[x][0]  # stored by the owner
+            # every unit whose range starts mid-tile emitted exactly one partial
+            emitted = t[4 * T:]
+            tbl = a.range_table()
+            expect = ((tbl[:, 0] % a.grid.iters_per_tile != 0) & (tbl[:, 1] > tbl[:, 0])).astype(int)
+            assert np.array_equal(emitted, expect), strat
+
+
+def test_large_square_checksums(sk, torch_cuda):
+    """8192^3 (BASELINE config 2): size-independent properties on integer-valued
+    operands in [-2, 1]: row/column checksums exact, sampled rows exact."""
+    torch = torch_cuda
+    m = n = k = 8192
+    blk = sk.kernel_blocking()
+    g = torch.Generator(device="cuda").manual_seed(1)
+    A = torch.randint(-2, 2, (m, k), device="cuda", generator=g).to(torch.bfloat16)
+    B = torch.randint(-2, 2, (k, n), device="cuda", generator=g).to(torch.bfloat16)
+    ones = torch.ones(n, 1, device="cuda", dtype=torch.float64)
+    rows = (A.double() @ (B.double() @ ones)).squeeze(1)
+    cols = ((torch.ones(1, m, device="cuda", dtype=torch.float64) @ A.double()) @ B.double()).squeeze(0)
+    sample = torch.arange(0, m, 997, device="cuda")
+    exact_rows = A[sample].double() @ B.double()
+    for a in (sk.stream_k(sk.GemmProblem(m, n, k), blk, 148),
+              sk.hybrid(sk.GemmProblem(m, n, k), blk, 148, sk.HybridVariant.TwoTileSkDp),
+              sk.data_parallel(sk.GemmProblem(m, n, k), blk)):
+        C = torch.empty(m, n, device="cuda")
+        gemm = sk.Gemm(a)
+        gemm.run(A, B, C)
+        gemm.check()
+        assert torch.equal(C.double().sum(1), rows)
+        assert torch.equal(C.double().sum(0), cols)
+        assert torch.equal(C[sample].double(), exact_rows)
