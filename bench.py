@@ -28,7 +28,6 @@ import json
 import math
 import os
 import statistics
-import subprocess
 import sys
 import time
 
@@ -51,7 +50,7 @@ def parse():
     ap.add_argument("--n", type=int, default=8192)
     ap.add_argument("--k", type=int, default=8192)
     ap.add_argument("--dtype", default="bf16", choices=["bf16", "fp16"])
-    ap.add_argument("--variant", default="auto", choices=["auto", "1sm", "2sm"])
+    ap.add_argument("--variant", default="2sm", choices=["auto", "1sm", "2sm"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-rows", type=int, default=0, help="row sample for the CPU legs (0=auto)")
@@ -80,45 +79,63 @@ def load_traffic(workload: str):
 
 
 class ClockSampler:
+    """SM clock + throttle reasons sampled DURING the timed region: an NVML
+    polling thread (~1 ms period), falling back to `nvidia-smi -lms 20`."""
+
+    REASONS = {  # nvmlClocksEventReason bits
+        0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+        0x4: "sw_power_cap",
+    }
+
     def __init__(self, index: int):
         self.index = index
-        self.proc = None
-        self.path = f"/tmp/sk_clocks_{os.getpid()}.csv"
+        self.samples = []
+        self.stop = False
+        self.thread = None
+        self.max_mhz = None
+
+    def _poll(self, nv, h):
+        while not self.stop:
+            try:
+                mhz = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                bits = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                pw = nv.nvmlDeviceGetPowerUsage(h) / 1000.0
+                self.samples.append((mhz, bits, pw))
+            except Exception:
+                pass
+            time.sleep(0.001)
 
     def __enter__(self):
+        import threading
+
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index),
-                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
-            time.sleep(0.3)
+            import pynvml as nv
+
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            self.thread = threading.Thread(target=self._poll, args=(nv, h), daemon=True)
+            self.thread.start()
+            time.sleep(0.01)
         except Exception:
-            self.proc = None
+            self.thread = None
         return self
 
     def __exit__(self, *exc):
-        if self.proc:
-            self.proc.terminate()
-            self.proc.wait()
+        self.stop = True
+        if self.thread:
+            self.thread.join()
 
     def summary(self):
-        try:
-            rows = [l.split(",") for l in open(self.path).read().strip().splitlines()]
-            rows = [[x.strip() for x in r] for r in rows if len(r) >= 8]
-        except Exception:
-            rows = []
-        if not rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in rows]
-        loaded = [s for s in sm if s > 500] or sm
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": float(rows[0][1]),
-                "reasons": reasons, "samples": len(rows),
-                "power_w_max": max(float(r[2]) for r in rows if r[2] not in ("[N/A]", ""))}
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"]}
+        sm = [s[0] for s in self.samples]
+        loaded = [x for x in sm if x > 500] or sm
+        reasons = sorted({name for _, bits, _ in self.samples for bit, name in self.REASONS.items()
+                          if bits & bit})
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": self.max_mhz, "reasons": reasons,
+                "samples": len(sm), "power_w_max": max(s[2] for s in self.samples),
+                "source": "NVML poll during the timed region"}
 
 
 def cpu_reference_leg(args, strategy, param, blk, rows=None):
@@ -133,7 +150,7 @@ def cpu_reference_leg(args, strategy, param, blk, rows=None):
     kind = "reference" if oracle.have_reference() else "port"
     orc = oracle.Oracle(kind)
     threads = os.cpu_count() or 1
-    rows = rows or args.cpu_rows or 256
+    rows = rows or args.cpu_rows or 3072
     m, n, k = rows, args.n, args.k
     A = orc.random_matrix(m, k, 42, "float32")
     B = orc.random_matrix(k, n, 43, "float32")
@@ -151,9 +168,10 @@ def cpu_reference_leg(args, strategy, param, blk, rows=None):
 def run_reference_arm(args, rank, world):
     if rank != 0:
         return
-    blk = (128, 256, 64)
+    # same tile config and grid knob as our arm (kernel_blocking of the variant)
+    blk = (256, 256, 64) if args.variant == "2sm" else (128, 256, 64)
     strategy = STRATS[args.strategy]
-    param = args.param or (2 if strategy == 1 else 148)
+    param = args.param or (2 if strategy == 1 else (74 if args.variant == "2sm" else 148))
     vals = []
     last = None
     for i in range(args.warmup + args.steps):

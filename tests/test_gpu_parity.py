@@ -48,33 +48,48 @@ def test_smoke():
     __graft_entry__.smoke()
 
 
+VARIANTS = ["1sm", "2sm"]
+
+
+def variant(sk, name):
+    return sk.Variant.OneSM if name == "1sm" else sk.Variant.TwoSM
+
+
+@pytest.mark.parametrize("var", VARIANTS)
 @pytest.mark.parametrize("shape", [(128, 256, 64), (384, 768, 1000), (129, 257, 65),
                                    (1000, 1000, 520), (256, 512, 4096), (640, 1280, 192)])
-def test_int_bit_exact_all_strategies_execute(sk, port, shape):
+def test_int_bit_exact_all_strategies_execute(sk, port, shape, var):
     m, n, k = shape
-    blk = sk.kernel_blocking()
+    V = variant(sk, var)
+    blk = sk.kernel_blocking(sk.DType.BFloat16, V)
     A, B = int_operands(port, m, n, k, 1234 + m)
     want = port.execute("data_parallel", 1, A, B, blk.blk_m, blk.blk_n, blk.blk_k).astype(np.float32)
     Af, Bf = A.astype(np.float32), B.astype(np.float32)
-    for a in strategies(sk, sk.GemmProblem(m, n, k), blk):
-        got = sk.execute(a, Af, Bf, compute=sk.DType.BFloat16)
+    p = 148 if V == sk.Variant.OneSM else 74
+    for a in strategies(sk, sk.GemmProblem(m, n, k), blk, p):
+        got = sk.execute(a, Af, Bf, compute=sk.DType.BFloat16, variant=V)
         assert np.array_equal(got, want), (sk.strategy_name(a.strategy), a.param)
 
 
-def test_int_bit_exact_fp16(sk, port):
+@pytest.mark.parametrize("var", VARIANTS)
+def test_int_bit_exact_fp16(sk, port, var):
     m, n, k = 512, 768, 640
-    blk = sk.kernel_blocking(sk.DType.Float16)
+    V = variant(sk, var)
+    blk = sk.kernel_blocking(sk.DType.Float16, V)
     A, B = int_operands(port, m, n, k, 77)
     want = (A @ B).astype(np.float32)
     for a in strategies(sk, sk.GemmProblem(m, n, k), blk):
-        got = sk.execute(a, A.astype(np.float16), B.astype(np.float16), compute=sk.DType.Float16)
+        got = sk.execute(a, A.astype(np.float16), B.astype(np.float16), compute=sk.DType.Float16,
+                         variant=V)
         assert np.array_equal(got, want), sk.strategy_name(a.strategy)
 
 
-def test_edge_schedules_bit_exact(sk, port):
+@pytest.mark.parametrize("var", VARIANTS)
+def test_edge_schedules_bit_exact(sk, port, var):
     """g > total_iters (empty units), one deep-k tile split 148 ways, the
     pathological DpOneTileSk (150 tiles, p=148: 20 empty ranges, 64 peers)."""
-    blk = sk.kernel_blocking()
+    V = variant(sk, var)
+    blk = sk.kernel_blocking(sk.DType.BFloat16, V)
     cases = [
         (sk.GemmProblem(128, 256, 128), lambda p: sk.stream_k(p, blk, 148)),
         (sk.GemmProblem(128, 256, 16384), lambda p: sk.stream_k(p, blk, 148)),
@@ -87,36 +102,40 @@ def test_edge_schedules_bit_exact(sk, port):
         # values in [-8, 7]: |partial sums| <= 64 * 16384 < 2^24, exact in fp32
         A, B = int_operands(port, problem.m, problem.n, problem.k, 99, shift=3)
         want = (A.astype(np.float64) @ B.astype(np.float64)).astype(np.float32)  # exact
-        got = sk.execute(a, A.astype(np.float32), B.astype(np.float32))
+        got = sk.execute(a, A.astype(np.float32), B.astype(np.float32), variant=V)
         assert np.array_equal(got, want), (problem, sk.strategy_name(a.strategy))
 
 
-def test_float_within_reference_bound(sk, port):
+@pytest.mark.parametrize("var", VARIANTS)
+def test_float_within_reference_bound(sk, port, var):
     m, n, k = 768, 1024, 2000
-    blk = sk.kernel_blocking()
+    V = variant(sk, var)
+    blk = sk.kernel_blocking(sk.DType.BFloat16, V)
     A = to_bf16_f32(port.random_matrix(m, k, 42, "float32"))
     B = to_bf16_f32(port.random_matrix(k, n, 43, "float32"))
     ref = port.gemm_reference(A, B, blk.blk_m, blk.blk_n, blk.blk_k)
     import oracle
 
     for a in strategies(sk, sk.GemmProblem(m, n, k), blk):
-        got = sk.execute(a, A, B)
+        got = sk.execute(a, A, B, variant=V)
         ok, max_abs, max_rel = oracle.verify(got, ref, k, EPS32)
         assert ok, (sk.strategy_name(a.strategy), max_abs, max_rel)
 
 
-def test_device_path_deterministic_and_self_cleaning(sk, torch_cuda):
+@pytest.mark.parametrize("var", VARIANTS)
+def test_device_path_deterministic_and_self_cleaning(sk, torch_cuda, var):
     torch = torch_cuda
     m = n = 2048
     k = 4096
-    blk = sk.kernel_blocking()
+    V = variant(sk, var)
+    blk = sk.kernel_blocking(sk.DType.BFloat16, V)
     g = torch.Generator(device="cuda").manual_seed(0)
     A = torch.rand(m, k, device="cuda", generator=g).mul_(2).sub_(1).to(torch.bfloat16)
     B = torch.rand(k, n, device="cuda", generator=g).mul_(2).sub_(1).to(torch.bfloat16)
     ref = A.double() @ B.double()
     for a in (sk.stream_k(sk.GemmProblem(m, n, k), blk, 148),
               sk.hybrid(sk.GemmProblem(m, n, k), blk, 148, sk.HybridVariant.DpOneTileSk)):
-        gemm = sk.Gemm(a)
+        gemm = sk.Gemm(a, variant=V)
         outs = []
         for _ in range(5):
             C = torch.full((m, n), float("nan"), device="cuda")
@@ -133,16 +152,18 @@ def test_device_path_deterministic_and_self_cleaning(sk, torch_cuda):
         assert int(flags.abs().sum()) == 0
 
 
-def test_trace_ownership_equals_fixup_peers_of(sk, torch_cuda):
+@pytest.mark.parametrize("var", VARIANTS)
+def test_trace_ownership_equals_fixup_peers_of(sk, torch_cuda, var):
     torch = torch_cuda
-    blk = sk.kernel_blocking()
+    V = variant(sk, var)
+    blk = sk.kernel_blocking(sk.DType.BFloat16, V)
     for problem, p in ((sk.GemmProblem(1024, 1024, 32768), 148), (sk.GemmProblem(1280, 3840, 512), 148),
                        (sk.GemmProblem(2048, 2048, 1024), 37)):
         for strat in (sk.Strategy.StreamK, sk.Strategy.FixedSplit, sk.Strategy.DpOneTileSk,
                       sk.Strategy.TwoTileSkDp, sk.Strategy.DataParallel):
             param = {sk.Strategy.FixedSplit: 3, sk.Strategy.DataParallel: 1}.get(strat, p)
             a = sk._assignment(strat, problem, blk, param)
-            gemm = sk.Gemm(a, trace=True)
+            gemm = sk.Gemm(a, variant=V, trace=True)
             A = torch.zeros(problem.m, problem.k, dtype=torch.bfloat16, device="cuda")
             B = torch.zeros(problem.k, problem.n, dtype=torch.bfloat16, device="cuda")
             C = torch.empty(problem.m, problem.n, device="cuda")
@@ -162,12 +183,15 @@ def test_trace_ownership_equals_fixup_peers_of(sk, torch_cuda):
             assert np.array_equal(emitted, expect), strat
 
 
-def test_large_square_checksums(sk, torch_cuda):
+@pytest.mark.parametrize("var", VARIANTS)
+def test_large_square_checksums(sk, torch_cuda, var):
     """8192^3 (BASELINE config 2): size-independent properties on integer-valued
     operands in [-2, 1]: row/column checksums exact, sampled rows exact."""
     torch = torch_cuda
     m = n = k = 8192
-    blk = sk.kernel_blocking()
+    V = variant(sk, var)
+    blk = sk.kernel_blocking(sk.DType.BFloat16, V)
+    p = 148 if V == sk.Variant.OneSM else 74
     g = torch.Generator(device="cuda").manual_seed(1)
     A = torch.randint(-2, 2, (m, k), device="cuda", generator=g).to(torch.bfloat16)
     B = torch.randint(-2, 2, (k, n), device="cuda", generator=g).to(torch.bfloat16)
@@ -176,11 +200,11 @@ def test_large_square_checksums(sk, torch_cuda):
     cols = ((torch.ones(1, m, device="cuda", dtype=torch.float64) @ A.double()) @ B.double()).squeeze(0)
     sample = torch.arange(0, m, 997, device="cuda")
     exact_rows = A[sample].double() @ B.double()
-    for a in (sk.stream_k(sk.GemmProblem(m, n, k), blk, 148),
-              sk.hybrid(sk.GemmProblem(m, n, k), blk, 148, sk.HybridVariant.TwoTileSkDp),
+    for a in (sk.stream_k(sk.GemmProblem(m, n, k), blk, p),
+              sk.hybrid(sk.GemmProblem(m, n, k), blk, p, sk.HybridVariant.TwoTileSkDp),
               sk.data_parallel(sk.GemmProblem(m, n, k), blk)):
         C = torch.empty(m, n, device="cuda")
-        gemm = sk.Gemm(a)
+        gemm = sk.Gemm(a, variant=V)
         gemm.run(A, B, C)
         gemm.check()
         assert torch.equal(C.double().sum(1), rows)
