@@ -131,6 +131,12 @@ sk_status sk_fixup_peers(const sk_problem* problem, const sk_blocking* blocking,
                          int64_t capacity, int64_t* nnz);
 sk_status sk_quantization_efficiency(int64_t t, int64_t p, double* out);
 
+/* ---- geometry corpus (sweep.cpp:21-28, 79-86) ---------------------------- */
+/* The paper's log-sampled shape corpus in run_sweep order: out[4*i] =
+ * {m, n, k, matrix_seed} of sample i, dims = clamp(llround(exp(ln lo + u (ln hi -
+ * ln lo))), lo, hi) with u from SplitMix64(seed); matrix_seed = next(). */
+sk_status sk_corpus(uint64_t seed, int64_t count, int64_t lo, int64_t hi, uint64_t* out);
+
 /* ---- device GEMM -------------------------------------------------------- */
 /* The tile configuration the device kernel uses for an input type/variant. */
 sk_status sk_kernel_blocking(sk_dtype ab_type, sk_variant variant, sk_blocking* out);

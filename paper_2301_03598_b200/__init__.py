@@ -39,7 +39,7 @@ __all__ = [
     "TileCoords", "CtaRange", "WorkAssignment", "tile_grid", "iter_to_coords", "data_parallel",
     "fixed_split", "stream_k", "hybrid", "fixup_peers_of", "quantization_efficiency", "to_text",
     "from_text", "kernel_blocking", "execute", "Gemm", "ProtocolError", "UnsupportedError",
-    "CudaError", "lib",
+    "CudaError", "lib", "corpus",
 ]
 
 
@@ -108,6 +108,7 @@ _SIGS = {
     "sk_execute": (C.c_int, [_P(sk_problem), _P(sk_blocking), C.c_int, C.c_int64, C.c_int, C.c_int,
                              C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32]),
     "sk_execute_release": (None, []),
+    "sk_corpus": (C.c_int, [C.c_uint64, C.c_int64, C.c_int64, C.c_int64, C.c_void_p]),
 }
 
 
@@ -393,6 +394,14 @@ def _infer_param(a: WorkAssignment) -> int:
         if tbl.shape == want.shape and np.array_equal(tbl, want):
             return c
     return 0
+
+
+def corpus(seed: int = 0, count: int = 32824, lo: int = 128, hi: int = 8192) -> np.ndarray:
+    """The paper's log-sampled geometry corpus in run_sweep order
+    (sweep.cpp:79-86): [count][4] uint64 rows of (m, n, k, matrix_seed)."""
+    out = np.zeros((count, 4), np.uint64)
+    _check(lib().sk_corpus(seed, count, lo, hi, out.ctypes.data_as(C.c_void_p)), "corpus")
+    return out
 
 
 # ----------------------------------------------------------------------------- device GEMM

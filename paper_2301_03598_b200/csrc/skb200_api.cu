@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -328,6 +329,32 @@ sk_status sk_fixup_peers(const sk_problem* p, const sk_blocking* b, sk_strategy 
 sk_status sk_quantization_efficiency(int64_t t, int64_t p, double* out) {
   if (t < 1 || p < 1) return fail(SK_EINVAL, "quantization_efficiency: t, p >= 1");
   if (out) *out = static_cast<double>(t) / static_cast<double>(ceil_div(t, p) * p);
+  return SK_OK;
+}
+
+sk_status sk_corpus(uint64_t seed, int64_t count, int64_t lo, int64_t hi, uint64_t* out) {
+  if (count < 0 || lo < 1 || hi < lo || (count > 0 && !out))
+    return fail(SK_EINVAL, "sk_corpus: bad arguments");
+  uint64_t state = seed;
+  auto next = [&state]() {  // SplitMix64, matrix.hpp:39-53
+    uint64_t z = (state += 0x9e3779b97f4a7c15ULL);
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+  };
+  auto sample = [&](int64_t a, int64_t b) -> int64_t {  // sweep.cpp:21-28 log_sample
+    if (a == b) return a;
+    const double u = static_cast<double>(next() >> 11) * 0x1.0p-53;
+    const double v = std::exp(std::log(static_cast<double>(a)) +
+                              u * (std::log(static_cast<double>(b)) - std::log(static_cast<double>(a))));
+    return std::min(std::max(static_cast<int64_t>(std::llround(v)), a), b);
+  };
+  for (int64_t i = 0; i < count; ++i) {
+    out[4 * i + 0] = static_cast<uint64_t>(sample(lo, hi));
+    out[4 * i + 1] = static_cast<uint64_t>(sample(lo, hi));
+    out[4 * i + 2] = static_cast<uint64_t>(sample(lo, hi));
+    out[4 * i + 3] = next();
+  }
   return SK_OK;
 }
 

@@ -1,0 +1,212 @@
+"""Geometry sweep on B200: BASELINE configs 3 (quantisation-limited shapes) and
+5 (the paper's 32,824-shape log-sampled corpus), Stream-K vs data-parallel.
+
+    python -m paper_2301_03598_b200.sweep --shapes config3 --out sweep.csv
+    python -m paper_2301_03598_b200.sweep --shapes corpus --count 2000 --out sweep.csv
+    torchrun --nproc-per-node N -m paper_2301_03598_b200.sweep --shapes corpus ...
+
+Mirrors run_sweep (core/src/sweep.cpp:75-112): shapes in corpus order
+(sk_corpus == sweep.cpp:21-28,79-86), one CSV row per (shape, strategy) under a
+versioned header, deterministic except the measured columns.  The simulator
+columns (utilization, makespan) are replaced by measured device time.
+
+Each (shape, strategy) is timed as a CUDA graph of R launches cycling over R
+copies of the operands (R chosen so the copies exceed L2 where memory allows),
+best of 3 replays, CUDA events on the capture stream.
+
+Multi-GPU: shape i runs on rank i % world (one problem per GPU, no
+collective on the data path); rank 0 merges the per-rank CSV parts in input
+order after a barrier.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import sys
+
+import numpy as np
+
+import paper_2301_03598_b200 as sk
+
+SCHEMA = "# schema=sk_b200/1"
+COLUMNS = ["m", "n", "k", "t", "iters_per_tile", "strategy", "param", "g", "variant", "dtype",
+           "copies", "l2_cold", "time_us", "tflops"]
+L2_BYTES = 126 * 1024 * 1024
+
+CONFIG3 = [
+    (1024, 1024, 32768), (1280, 3840, 4096), (1280, 3840, 8192), (1024, 4864, 4096),
+    (2560, 3840, 4096), (1024, 1024, 8192), (512, 512, 65536), (3072, 3072, 3072),
+    (2304, 2304, 8192), (1280, 7680, 4096), (4096, 4096, 4096), (8192, 8192, 8192),
+]
+
+
+def strategies_for(problem, blk, p, names):
+    out = []
+    for name in names:
+        if name == "data_parallel":
+            out.append(sk.data_parallel(problem, blk))
+        elif name == "stream_k":
+            out.append(sk.stream_k(problem, blk, p))
+        elif name == "two_tile_sk_dp":
+            out.append(sk.hybrid(problem, blk, p, sk.HybridVariant.TwoTileSkDp))
+        elif name == "dp_one_tile_sk":
+            out.append(sk.hybrid(problem, blk, p, sk.HybridVariant.DpOneTileSk))
+        elif name == "fixed_split":
+            out.append(sk.fixed_split(problem, blk, 2))
+        else:
+            raise ValueError(name)
+    return out
+
+
+class ShapeTimer:
+    """Pitched operand copies for one shape + graph-timed launches."""
+
+    def __init__(self, torch, m, n, k, tdt, max_copies=16, mem_budget=4 << 30):
+        self.torch = torch
+        lda, ldb, ldc = -(-k // 8) * 8, -(-n // 8) * 8, -(-n // 4) * 4
+        foot = 2 * (m * lda + k * ldb)
+        self.copies = int(max(1, min(max_copies, math.ceil(2 * L2_BYTES / foot),
+                                     mem_budget // max(foot, 1))))
+        self.cold = self.copies * foot > L2_BYTES
+        g = torch.Generator(device="cuda").manual_seed(m * 131 + n * 7 + k)
+        self.A = [torch.empty(m, lda, device="cuda", dtype=tdt)[:, :k] for _ in range(self.copies)]
+        self.B = [torch.empty(k, ldb, device="cuda", dtype=tdt)[:, :n] for _ in range(self.copies)]
+        for t in self.A + self.B:
+            t.copy_(torch.rand(t.shape, device="cuda", generator=g) * 2 - 1)
+        self.C = torch.empty(m, ldc, device="cuda", dtype=torch.float32)[:, :n]
+
+    def time_us(self, gemm, reps=3):
+        torch = self.torch
+        for i in range(self.copies):  # warm-up + lazy attribute setup outside capture
+            gemm.run(self.A[i], self.B[i], self.C)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(graph, stream=s):
+                for i in range(self.copies):
+                    gemm.run(self.A[i], self.B[i], self.C)
+        torch.cuda.synchronize()
+        best = float("inf")
+        for _ in range(reps):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            graph.replay()
+            e1.record()
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1) * 1e3 / self.copies)
+        gemm.check()
+        return best
+
+
+def run(shapes, names, variant, dtype, rank=0, world=1, log_every=0):
+    import torch
+
+    ab = sk.DType.BFloat16 if dtype == "bf16" else sk.DType.Float16
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float16
+    blk = sk.kernel_blocking(ab, variant)
+    sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    p = sms // (2 if variant == sk.Variant.TwoSM else 1)
+    rows = []
+    for idx, (m, n, k) in enumerate(shapes):
+        if idx % world != rank:
+            continue
+        problem = sk.GemmProblem(int(m), int(n), int(k))
+        timer = ShapeTimer(torch, int(m), int(n), int(k), tdt)
+        for a in strategies_for(problem, blk, p, names):
+            gemm = sk.Gemm(a, ab, variant)
+            t = timer.time_us(gemm)
+            rows.append({"idx": idx, "m": m, "n": n, "k": k, "t": a.grid.total_tiles,
+                         "iters_per_tile": a.grid.iters_per_tile,
+                         "strategy": sk.strategy_name(a.strategy), "param": a.param,
+                         "g": a.grid_size, "variant": "2sm" if variant == sk.Variant.TwoSM else "1sm",
+                         "dtype": dtype, "copies": timer.copies, "l2_cold": int(timer.cold),
+                         "time_us": t, "tflops": 2.0 * m * n * k / (t * 1e-6) / 1e12})
+        del timer
+        if log_every and (idx // world) % log_every == 0:
+            print(f"[rank {rank}] {idx}/{len(shapes)} {m}x{n}x{k}", file=sys.stderr, flush=True)
+    return rows
+
+
+def summarise(rows, names, baseline="data_parallel", tol=0.05):
+    """Geomean TFLOP/s speedup of each strategy over data-parallel, plus the
+    'best Stream-K family' oracle selection and regressions beyond `tol`."""
+    by_shape = {}
+    for r in rows:
+        by_shape.setdefault(r["idx"], {})[r["strategy"]] = r["time_us"]
+    out = {"shapes": len(by_shape)}
+    for name in names:
+        if name == baseline:
+            continue
+        sp = [d[baseline] / d[name] for d in by_shape.values() if name in d and baseline in d]
+        if sp:
+            out[name] = {"geomean_speedup": float(np.exp(np.mean(np.log(sp)))),
+                         "min": float(min(sp)), "max": float(max(sp)),
+                         "regress_gt_5pct": int(sum(s < 1 - tol for s in sp))}
+    return out
+
+
+def write_csv(path, rows):
+    rows = sorted(rows, key=lambda r: (r["idx"], r["strategy"]))
+    with open(path, "w") as f:
+        f.write(SCHEMA + "\n" + ",".join(COLUMNS) + "\n")
+        for r in rows:
+            f.write(",".join(f"{r[c]:.6g}" if isinstance(r[c], float) else str(r[c]) for c in COLUMNS)
+                    + "\n")
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--shapes", default="config3", choices=["config3", "corpus"])
+    ap.add_argument("--count", type=int, default=32824)
+    ap.add_argument("--offset", type=int, default=0)
+    ap.add_argument("--lo", type=int, default=128)
+    ap.add_argument("--hi", type=int, default=8192)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--variant", default="2sm", choices=["1sm", "2sm"])
+    ap.add_argument("--dtype", default="bf16", choices=["bf16", "fp16"])
+    ap.add_argument("--strategies", default="data_parallel,stream_k,two_tile_sk_dp,dp_one_tile_sk")
+    ap.add_argument("--out", default="sweep.csv")
+    ap.add_argument("--log-every", type=int, default=0)
+    args = ap.parse_args(argv)
+
+    import torch
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+    if args.shapes == "config3":
+        shapes = CONFIG3
+    else:
+        c = sk.corpus(args.seed, args.offset + args.count, args.lo, args.hi)[args.offset:]
+        shapes = [tuple(int(x) for x in r[:3]) for r in c]
+    names = args.strategies.split(",")
+    variant = sk.Variant.TwoSM if args.variant == "2sm" else sk.Variant.OneSM
+    rows = run(shapes, names, variant, args.dtype, rank, world, args.log_every)
+    part = f"{args.out}.part{rank}.json"
+    with open(part, "w") as f:
+        json.dump(rows, f)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("gloo")
+        dist.barrier()  # control plane only: every part is on disk
+    if rank == 0:
+        allrows = []
+        for r in range(world):
+            with open(f"{args.out}.part{r}.json") as f:
+                allrows += json.load(f)
+            os.remove(f"{args.out}.part{r}.json")
+        write_csv(args.out, allrows)
+        print(json.dumps({"sweep": args.shapes, "variant": args.variant, "dtype": args.dtype,
+                          "world": world, **summarise(allrows, names)}))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
