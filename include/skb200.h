@@ -137,6 +137,23 @@ sk_status sk_quantization_efficiency(int64_t t, int64_t p, double* out);
  * ln lo))), lo, hi) with u from SplitMix64(seed); matrix_seed = next(). */
 sk_status sk_corpus(uint64_t seed, int64_t count, int64_t lo, int64_t hi, uint64_t* out);
 
+/* ---- grid-size model (costmodel.hpp:13-60, wave-aware) -------------------- */
+/* time(g) = e + ceil(g/p) * (a + b*[peers>1] + c*ipc + d*(peers-1)), microseconds. */
+typedef struct sk_cost_params {
+  double e, a, b, c, d;
+  double fit_residual;
+} sk_cost_params;
+/* B200-calibrated constants for a kernel family. */
+sk_status sk_default_cost_params(sk_dtype ab_type, sk_variant variant, sk_cost_params* out);
+sk_status sk_predict_time(const sk_cost_params* params, const sk_tile_grid_t* grid, int64_t g,
+                          int64_t p, double* out);
+/* argmin over g in {1..p} U {t} (costmodel.cpp:30-48); g == t is data-parallel. */
+sk_status sk_select_grid_size(const sk_cost_params* params, const sk_tile_grid_t* grid, int64_t p,
+                              int64_t* g);
+/* Non-negative least squares over n >= 5 measured (grid, g, time) samples. */
+sk_status sk_calibrate(const sk_tile_grid_t* grids, const int64_t* g, const double* times,
+                       int64_t n, int64_t p, sk_cost_params* out);
+
 /* ---- device GEMM -------------------------------------------------------- */
 /* The tile configuration the device kernel uses for an input type/variant. */
 sk_status sk_kernel_blocking(sk_dtype ab_type, sk_variant variant, sk_blocking* out);

@@ -109,6 +109,10 @@ _SIGS = {
                              C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32]),
     "sk_execute_release": (None, []),
     "sk_corpus": (C.c_int, [C.c_uint64, C.c_int64, C.c_int64, C.c_int64, C.c_void_p]),
+    "sk_default_cost_params": (C.c_int, [C.c_int, C.c_int, C.c_void_p]),
+    "sk_predict_time": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, _P(C.c_double)]),
+    "sk_select_grid_size": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, _P(C.c_int64)]),
+    "sk_calibrate": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_void_p]),
 }
 
 
@@ -394,6 +398,63 @@ def _infer_param(a: WorkAssignment) -> int:
         if tbl.shape == want.shape and np.array_equal(tbl, want):
             return c
     return 0
+
+
+class CostParams(C.Structure):
+    """costmodel.hpp:15-21 CostParams plus the launch term e (wave-aware model,
+    csrc/costmodel.cpp):  time(g) = e + ceil(g/p)*(a + b[peers>1] + c*ipc + d*(peers-1))."""
+    _fields_ = [("e", C.c_double), ("a", C.c_double), ("b", C.c_double), ("c", C.c_double),
+                ("d", C.c_double), ("fit_residual", C.c_double)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+def default_cost_params(ab_type: "DType" = None, variant: "Variant" = None) -> CostParams:
+    ab_type = DType.BFloat16 if ab_type is None else ab_type
+    variant = Variant.TwoSM if variant is None else variant
+    out = CostParams()
+    _check(lib().sk_default_cost_params(int(ab_type), int(variant), C.byref(out)), "cost params")
+    return out
+
+
+def predict_time(params: CostParams, grid: "TileGrid", g: int, p: int) -> float:
+    out = C.c_double()
+    _check(lib().sk_predict_time(C.byref(params), C.byref(grid._c()), g, p, C.byref(out)),
+           "predict_time")
+    return out.value
+
+
+def select_grid_size(params: CostParams, grid: "TileGrid", p: int) -> int:
+    """costmodel.cpp:30-48 argmin over g in {1..p} U {t}; g == t means data-parallel."""
+    out = C.c_int64()
+    _check(lib().sk_select_grid_size(C.byref(params), C.byref(grid._c()), p, C.byref(out)),
+           "select_grid_size")
+    return out.value
+
+
+def calibrate(samples, p: int) -> CostParams:
+    """NNLS fit from [(TileGrid, g, time_us), ...] (costmodel.cpp:142-225)."""
+    n = len(samples)
+    grids = (sk_tile_grid_t * n)(*[s[0]._c() for s in samples])
+    gs = np.array([s[1] for s in samples], np.int64)
+    ts = np.array([s[2] for s in samples], np.float64)
+    out = CostParams()
+    _check(lib().sk_calibrate(grids, gs.ctypes.data_as(C.c_void_p), ts.ctypes.data_as(C.c_void_p),
+                              n, p, C.byref(out)), "calibrate")
+    return out
+
+
+def auto_stream_k(problem: "GemmProblem", blocking: "BlockingFactors", p: int,
+                  params: Optional[CostParams] = None) -> "WorkAssignment":
+    """stream_k with the model-selected grid size (the paper's Stream-K policy);
+    g == t returns the equivalent data-parallel schedule (stream_k(t) == DP)."""
+    params = params or default_cost_params()
+    grid = tile_grid(problem, blocking)
+    g = select_grid_size(params, grid, p)
+    if g == min(grid.total_tiles, grid.total_iters) and grid.total_tiles <= grid.total_iters:
+        return data_parallel(problem, blocking)
+    return stream_k(problem, blocking, g)
 
 
 def corpus(seed: int = 0, count: int = 32824, lo: int = 128, hi: int = 8192) -> np.ndarray:

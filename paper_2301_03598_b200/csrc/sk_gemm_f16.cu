@@ -150,6 +150,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if constexpr (CG == 2) cluster_sync();  // peer barriers initialised before any remote use
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_base_smem;
+  // Programmatic dependent launch: the prologue above overlaps the previous
+  // kernel's tail; nothing below touches global memory before it completes.
+  ptx::grid_dependency_wait();
+  ptx::launch_dependents();
 
   if (warp == 0) {
     // ===================== TMA producer (every CTA of the pair) =====================
@@ -254,45 +258,56 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         __syncwarp();
       }
       float* my_slab = partial ? partials + fidx(u) * static_cast<int64_t>(SLAB_ELEMS) : nullptr;
+      // 64 columns (two 32-column chunks) per step: one tcgen05.ld.x64, 16 float4
+      // of peer slab in flight per thread, two 32x32 TMA-store boxes.
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
-        float v[32];
-        ptx::tmem_ld32(tsrc + c * 32, v);
+      for (int c = 0; c < BN / 32; c += 2) {
+        float v[64];
+        ptx::tmem_ld64(tsrc + c * 32, v);
         if (partial) {
 #pragma unroll
-          for (int j = 0; j < 8; ++j)
-            ptx::st_cg_f4(slab_ptr(my_slab, c, j, row),
+          for (int j = 0; j < 16; ++j)
+            ptx::st_cg_f4(slab_ptr(my_slab, c + j / 8, j % 8, row),
                           make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
         } else {
           // Owner fold: own accumulator, then peers in ascending id (executor.hpp:165-172).
 #pragma unroll 1
           for (int p = 1; p <= npeer; ++p) {
             float* ps = partials + fidx(u + p) * static_cast<int64_t>(SLAB_ELEMS);
+            float4 w[16];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              const float4 w = ptx::ld_cg_f4(slab_ptr(ps, c, j, row));
-              v[4 * j] += w.x;
-              v[4 * j + 1] += w.y;
-              v[4 * j + 2] += w.z;
-              v[4 * j + 3] += w.w;
+            for (int j = 0; j < 16; ++j) w[j] = ptx::ld_cg_f4(slab_ptr(ps, c + j / 8, j % 8, row));
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              v[4 * j] += w[j].x;
+              v[4 * j + 1] += w[j].y;
+              v[4 * j + 2] += w[j].z;
+              v[4 * j + 3] += w[j].w;
             }
           }
           // Stage through swizzled smem (16-B chunk j of row r at j ^ (r % 8)), TMA store.
-          float* buf = stage_buf + (nstores & 1) * (EPI_BUF_BYTES / 4);
-          if (nstores >= 2) {
-            if (lane == 0) ptx::tma_store_wait_read<1>();
+          if (nstores > 0) {
+            if (lane == 0) ptx::tma_store_wait_read<0>();
             __syncwarp();
           }
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const int jj = j ^ static_cast<int>(lane & 7);
-            *reinterpret_cast<float4*>(buf + lane * 32 + jj * 4) =
-                make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          for (int h = 0; h < 2; ++h) {
+            float* buf = stage_buf + h * (EPI_BUF_BYTES / 4);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const int jj = j ^ static_cast<int>(lane & 7);
+              *reinterpret_cast<float4*>(buf + lane * 32 + jj * 4) =
+                  make_float4(v[32 * h + 4 * j], v[32 * h + 4 * j + 1], v[32 * h + 4 * j + 2],
+                              v[32 * h + 4 * j + 3]);
+            }
           }
           ptx::fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
-            ptx::tma_store_2d(&tmC, buf, n0 + c * 32, m0 + static_cast<int32_t>(q * 32));
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+              ptx::tma_store_2d(&tmC, stage_buf + h * (EPI_BUF_BYTES / 4), n0 + (c + h) * 32,
+                                m0 + static_cast<int32_t>(q * 32));
             ptx::tma_store_commit();
           }
           ++nstores;
@@ -374,13 +389,15 @@ static cudaError_t launch_cg(const CUtensorMap& a, const CUtensorMap& b, const C
   cfg.blockDim = dim3(f16::NUM_THREADS);
   cfg.dynamicSmemBytes = f16::Cfg<CG>::alloc;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = CG;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   return cudaLaunchKernelEx(&cfg, kern, a, b, c, p);
 }
 

@@ -31,7 +31,8 @@ import numpy as np
 import paper_2301_03598_b200 as sk
 
 SCHEMA = "# schema=sk_b200/1"
-COLUMNS = ["m", "n", "k", "t", "iters_per_tile", "strategy", "param", "g", "variant", "dtype",
+COLUMNS = ["m", "n", "k", "tiles_m", "tiles_n", "t", "iters_per_tile", "strategy", "param", "g",
+           "variant", "dtype",
            "copies", "l2_cold", "time_us", "tflops"]
 L2_BYTES = 126 * 1024 * 1024
 
@@ -42,13 +43,30 @@ CONFIG3 = [
 ]
 
 
-def strategies_for(problem, blk, p, names):
+def strategies_for(problem, blk, p, names, params=None):
+    """Strategy tokens: data_parallel, stream_k (g = p), stream_k:<g>,
+    stream_k:auto (model-selected g, cost model in csrc/costmodel.cpp),
+    stream_k:cal (calibration set: g in {p, p/2, p/4, p/8, p/16}), two_tile_sk_dp,
+    dp_one_tile_sk, fixed_split."""
     out = []
     for name in names:
         if name == "data_parallel":
             out.append(sk.data_parallel(problem, blk))
         elif name == "stream_k":
             out.append(sk.stream_k(problem, blk, p))
+        elif name == "stream_k:auto":
+            a = sk.auto_stream_k(problem, blk, p, params)
+            a.label = "stream_k:auto"
+            out.append(a)
+        elif name == "stream_k:cal":
+            for g in sorted({max(1, p >> i) for i in range(5)}, reverse=True):
+                a = sk.stream_k(problem, blk, g)
+                a.label = f"stream_k:{g}"
+                out.append(a)
+        elif name.startswith("stream_k:"):
+            a = sk.stream_k(problem, blk, int(name.split(":")[1]))
+            a.label = name
+            out.append(a)
         elif name == "two_tile_sk_dp":
             out.append(sk.hybrid(problem, blk, p, sk.HybridVariant.TwoTileSkDp))
         elif name == "dp_one_tile_sk":
@@ -102,7 +120,7 @@ class ShapeTimer:
         return best
 
 
-def run(shapes, names, variant, dtype, rank=0, world=1, log_every=0):
+def run(shapes, names, variant, dtype, rank=0, world=1, log_every=0, params=None):
     import torch
 
     ab = sk.DType.BFloat16 if dtype == "bf16" else sk.DType.Float16
@@ -110,18 +128,20 @@ def run(shapes, names, variant, dtype, rank=0, world=1, log_every=0):
     blk = sk.kernel_blocking(ab, variant)
     sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
     p = sms // (2 if variant == sk.Variant.TwoSM else 1)
+    params = params or sk.default_cost_params(ab, variant)
     rows = []
     for idx, (m, n, k) in enumerate(shapes):
         if idx % world != rank:
             continue
         problem = sk.GemmProblem(int(m), int(n), int(k))
         timer = ShapeTimer(torch, int(m), int(n), int(k), tdt)
-        for a in strategies_for(problem, blk, p, names):
+        for a in strategies_for(problem, blk, p, names, params):
             gemm = sk.Gemm(a, ab, variant)
             t = timer.time_us(gemm)
             rows.append({"idx": idx, "m": m, "n": n, "k": k, "t": a.grid.total_tiles,
                          "iters_per_tile": a.grid.iters_per_tile,
-                         "strategy": sk.strategy_name(a.strategy), "param": a.param,
+                         "strategy": getattr(a, "label", sk.strategy_name(a.strategy)),
+                         "param": a.param, "tiles_m": a.grid.tiles_m, "tiles_n": a.grid.tiles_n,
                          "g": a.grid_size, "variant": "2sm" if variant == sk.Variant.TwoSM else "1sm",
                          "dtype": dtype, "copies": timer.copies, "l2_cold": int(timer.cold),
                          "time_us": t, "tflops": 2.0 * m * n * k / (t * 1e-6) / 1e12})
@@ -131,22 +151,35 @@ def run(shapes, names, variant, dtype, rank=0, world=1, log_every=0):
     return rows
 
 
-def summarise(rows, names, baseline="data_parallel", tol=0.05):
-    """Geomean TFLOP/s speedup of each strategy over data-parallel, plus the
-    'best Stream-K family' oracle selection and regressions beyond `tol`."""
+def summarise(rows, baseline="data_parallel", tol=0.05):
+    """Geomean TFLOP/s speedup of each strategy over data-parallel (per-shape
+    time ratio), its range, and the shapes regressing beyond `tol`."""
     by_shape = {}
     for r in rows:
         by_shape.setdefault(r["idx"], {})[r["strategy"]] = r["time_us"]
+    labels = sorted({r["strategy"] for r in rows} - {baseline})
     out = {"shapes": len(by_shape)}
-    for name in names:
-        if name == baseline:
-            continue
+    for name in labels:
         sp = [d[baseline] / d[name] for d in by_shape.values() if name in d and baseline in d]
         if sp:
             out[name] = {"geomean_speedup": float(np.exp(np.mean(np.log(sp)))),
                          "min": float(min(sp)), "max": float(max(sp)),
                          "regress_gt_5pct": int(sum(s < 1 - tol for s in sp))}
     return out
+
+
+def fit_cost_model(rows, p):
+    """Calibrate the wave-aware model on measured rows (stream_k:<g> and
+    data_parallel) and report its selection quality."""
+    samples = []
+    for r in rows:
+        if r["strategy"] == "data_parallel" or r["strategy"].startswith("stream_k:") and \
+                r["strategy"] != "stream_k:auto":
+            grid = sk.TileGrid(r["tiles_m"], r["tiles_n"], r["t"], r["iters_per_tile"],
+                               r["t"] * r["iters_per_tile"])
+            samples.append((grid, r["g"], r["time_us"]))
+    params = sk.calibrate(samples, p)
+    return params, len(samples)
 
 
 def write_csv(path, rows):
@@ -171,6 +204,8 @@ def main(argv=None):
     ap.add_argument("--strategies", default="data_parallel,stream_k,two_tile_sk_dp,dp_one_tile_sk")
     ap.add_argument("--out", default="sweep.csv")
     ap.add_argument("--log-every", type=int, default=0)
+    ap.add_argument("--calibrate", action="store_true",
+                    help="fit the grid-size model on the measured stream_k:<g>/data_parallel rows")
     args = ap.parse_args(argv)
 
     import torch
@@ -201,8 +236,15 @@ def main(argv=None):
                 allrows += json.load(f)
             os.remove(f"{args.out}.part{r}.json")
         write_csv(args.out, allrows)
-        print(json.dumps({"sweep": args.shapes, "variant": args.variant, "dtype": args.dtype,
-                          "world": world, **summarise(allrows, names)}))
+        summary = {"sweep": args.shapes, "variant": args.variant, "dtype": args.dtype,
+                   "world": world, **summarise(allrows)}
+        if args.calibrate:
+            p = torch.cuda.get_device_properties(0).multi_processor_count // (
+                2 if args.variant == "2sm" else 1)
+            params, n = fit_cost_model(allrows, p)
+            summary["cost_params"] = params.as_dict()
+            summary["calibration_samples"] = n
+        print(json.dumps(summary))
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
