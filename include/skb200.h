@@ -138,9 +138,13 @@ sk_status sk_quantization_efficiency(int64_t t, int64_t p, double* out);
 sk_status sk_corpus(uint64_t seed, int64_t count, int64_t lo, int64_t hi, uint64_t* out);
 
 /* ---- grid-size model (costmodel.hpp:13-60, wave-aware) -------------------- */
-/* time(g) = e + ceil(g/p) * (a + b*[peers>1] + c*ipc + d*(peers-1)), microseconds. */
+/* time(g) = e + ceil(g/p) * (a + b*[peers>1] + c*ipc + d*(peers-1) + s*segs), microseconds;
+ * segs = tile segments per unit.  margin: minimum predicted Stream-K gain over
+ * data-parallel before select_grid_size leaves g = t.  sk_calibrate keeps the
+ * caller's margin and writes the RMS relative fit error to fit_residual. */
 typedef struct sk_cost_params {
-  double e, a, b, c, d;
+  double e, a, b, c, d, s;
+  double margin;
   double fit_residual;
 } sk_cost_params;
 /* B200-calibrated constants for a kernel family. */

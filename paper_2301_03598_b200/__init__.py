@@ -401,10 +401,12 @@ def _infer_param(a: WorkAssignment) -> int:
 
 
 class CostParams(C.Structure):
-    """costmodel.hpp:15-21 CostParams plus the launch term e (wave-aware model,
-    csrc/costmodel.cpp):  time(g) = e + ceil(g/p)*(a + b[peers>1] + c*ipc + d*(peers-1))."""
+    """costmodel.hpp:15-21 CostParams plus B200 terms (csrc/costmodel.cpp):
+    time(g) = e + ceil(g/p)*(a + b[peers>1] + c*ipc + d*(peers-1) + s*segs);
+    `margin` = minimum predicted gain before leaving data-parallel."""
     _fields_ = [("e", C.c_double), ("a", C.c_double), ("b", C.c_double), ("c", C.c_double),
-                ("d", C.c_double), ("fit_residual", C.c_double)]
+                ("d", C.c_double), ("s", C.c_double), ("margin", C.c_double),
+                ("fit_residual", C.c_double)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -433,13 +435,14 @@ def select_grid_size(params: CostParams, grid: "TileGrid", p: int) -> int:
     return out.value
 
 
-def calibrate(samples, p: int) -> CostParams:
+def calibrate(samples, p: int, margin: float = 0.15) -> CostParams:
     """NNLS fit from [(TileGrid, g, time_us), ...] (costmodel.cpp:142-225)."""
     n = len(samples)
     grids = (sk_tile_grid_t * n)(*[s[0]._c() for s in samples])
     gs = np.array([s[1] for s in samples], np.int64)
     ts = np.array([s[2] for s in samples], np.float64)
     out = CostParams()
+    out.margin = margin
     _check(lib().sk_calibrate(grids, gs.ctypes.data_as(C.c_void_p), ts.ctypes.data_as(C.c_void_p),
                               n, p, C.byref(out)), "calibrate")
     return out

@@ -54,6 +54,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         "-Xlinker", "--version-script=" + os.path.join(CSRC, "exports.map"),
         "-Xcompiler", "-static-libstdc++", "-Xcompiler", "-static-libgcc",
         "-cudart", "static",
+        *os.environ.get("SKB200_DEFINES", "").split(),
         *[os.path.join(CSRC, f) for f in SOURCES],
         "-o", tmp,
     ]

@@ -275,6 +275,10 @@ __device__ __forceinline__ void st_cg_f4(float4* p, float4 v) {
                "f"(v.z), "f"(v.w)
                : "memory");
 }
+// Invalidate one 128-B L2 line without writing it back (contents become undefined).
+__device__ __forceinline__ void discard_l2(const void* p) {
+  asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
+}
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }

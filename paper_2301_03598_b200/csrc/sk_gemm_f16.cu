@@ -42,8 +42,12 @@ constexpr int BN = 256;    // tile columns (MMA N)
 constexpr int BK = 64;
 constexpr int UMMA_K = 16;
 constexpr int EPI_WARPS = 4;
+#ifndef SKB200_EPI_BUFS
+#define SKB200_EPI_BUFS 2
+#endif
+constexpr int EPI_BUFS = SKB200_EPI_BUFS;   // 4-KB TMA-store staging boxes per epilogue warp
 constexpr int EPI_BUF_BYTES = 32 * 32 * 4;  // 32 rows x 32 fp32 = 4 KB
-constexpr int EPI_BYTES = EPI_WARPS * 2 * EPI_BUF_BYTES;
+constexpr int EPI_BYTES = EPI_WARPS * EPI_BUFS * EPI_BUF_BYTES;
 constexpr int NUM_THREADS = 64 + 32 * EPI_WARPS;  // 192
 constexpr int TMEM_COLS = 512;                    // 2 x 256-col accumulators
 constexpr int SLAB_ELEMS = ROWS * BN;             // fp32 partial per CTA rank
@@ -55,7 +59,13 @@ struct Cfg {
   static constexpr int A_STAGE = ROWS * BK * 2;             // 16 KB
   static constexpr int B_STAGE = B_COLS * BK * 2;           // 32 KB (1-SM) / 16 KB (2-SM)
   static constexpr int STAGE = A_STAGE + B_STAGE;
-  static constexpr int STAGES = CG == 1 ? 4 : 6;
+#ifndef SKB200_STAGES_1SM
+#define SKB200_STAGES_1SM 4
+#endif
+#ifndef SKB200_STAGES_2SM
+#define SKB200_STAGES_2SM 6
+#endif
+  static constexpr int STAGES = CG == 1 ? SKB200_STAGES_1SM : SKB200_STAGES_2SM;
   static constexpr int a_off = 0;
   static constexpr int b_off = a_off + STAGES * A_STAGE;
   static constexpr int epi_off = b_off + STAGES * B_STAGE;
@@ -236,7 +246,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const uint32_t q = warp % 4;  // TMEM lane quarter this warp may access
     const int row = static_cast<int>(q * 32 + lane);
     const bool leader = (threadIdx.x == 64);
-    float* stage_buf = sEpi + (warp - 2) * 2 * (EPI_BUF_BYTES / 4);
+    float* stage_buf = sEpi + (warp - 2) * EPI_BUFS * (EPI_BUF_BYTES / 4);
     float* partials = static_cast<float*>(P.partials);
     uint32_t acc = 0, acc_phase = 0, nstores = 0;
     // flag / slab index of a (unit, rank): each CTA of a pair runs its own protocol
@@ -284,15 +294,24 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               v[4 * j + 2] += w[j].z;
               v[4 * j + 3] += w[j].w;
             }
-          }
-          // Stage through swizzled smem (16-B chunk j of row r at j ^ (r % 8)), TMA store.
-          if (nstores > 0) {
-            if (lane == 0) ptx::tma_store_wait_read<0>();
+            // The slab lines this warp just consumed are dead: drop them from L2
+            // without a DRAM write-back (one lane per 128-B line).
             __syncwarp();
+            if ((lane & 7) == 0) {
+#pragma unroll
+              for (int j = 0; j < 16; ++j) ptx::discard_l2(slab_ptr(ps, c + j / 8, j % 8, row));
+            }
           }
+          // Stage each 32-column half through a ring of EPI_BUFS swizzled smem boxes
+          // (16-B chunk j of row r at j ^ (r % 8)); EPI_BUFS - 1 TMA stores stay in
+          // flight while the next box is written.
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
-            float* buf = stage_buf + h * (EPI_BUF_BYTES / 4);
+            float* buf = stage_buf + (nstores % EPI_BUFS) * (EPI_BUF_BYTES / 4);
+            if (nstores >= EPI_BUFS) {
+              if (lane == 0) ptx::tma_store_wait_read<EPI_BUFS - 1>();
+              __syncwarp();
+            }
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
               const int jj = j ^ static_cast<int>(lane & 7);
@@ -300,17 +319,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                   make_float4(v[32 * h + 4 * j], v[32 * h + 4 * j + 1], v[32 * h + 4 * j + 2],
                               v[32 * h + 4 * j + 3]);
             }
+            ptx::fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              ptx::tma_store_2d(&tmC, buf, n0 + (c + h) * 32, m0 + static_cast<int32_t>(q * 32));
+              ptx::tma_store_commit();
+            }
+            ++nstores;
           }
-          ptx::fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) {
-#pragma unroll
-            for (int h = 0; h < 2; ++h)
-              ptx::tma_store_2d(&tmC, stage_buf + h * (EPI_BUF_BYTES / 4), n0 + (c + h) * 32,
-                                m0 + static_cast<int32_t>(q * 32));
-            ptx::tma_store_commit();
-          }
-          ++nstores;
         }
       }
       // Accumulator drained: hand the TMEM buffer back to the (leader's) MMA warp.
