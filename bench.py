@@ -53,6 +53,7 @@ def parse():
     ap.add_argument("--variant", default="2sm", choices=["auto", "1sm", "2sm"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--cpu-rows", type=int, default=0, help="row sample for the CPU legs (0=auto)")
     return ap.parse_args()
 
@@ -308,6 +309,19 @@ def main():
                "path": "sk_execute (C ABI, host buffers, pinned)"}
         sk.lib().sk_execute_release()
 
+    # Live Stream-K vs data-parallel geomean over BASELINE config 3's
+    # quantisation-limited shapes (the metric's second half; the full corpus
+    # is measured by `python -m paper_2301_03598_b200.sweep`).
+    sweep = None
+    if rank == 0 and not args.no_sweep:
+        from paper_2301_03598_b200 import sweep as sw
+
+        rows = sw.run(sw.CONFIG3, ["data_parallel", "stream_k:auto"], variant, args.dtype)
+        summ = sw.summarise(rows)["stream_k:auto"]
+        sweep = {"shapes": "config3 (%d)" % len(sw.CONFIG3), "policy": "stream_k:auto (cost model)",
+                 "geomean_sk_vs_dp": summ["geomean_speedup"], "min": summ["min"],
+                 "max": summ["max"], "regress_gt_5pct": summ["regress_gt_5pct"]}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         tf, dt, sample, cores, kind = cpu_reference_leg(args, int(strategy), param,
@@ -340,6 +354,7 @@ def main():
             "gpu_launches": args.steps,
             "e2e": e2e,
             "cpu_baseline": cpu,
+            "stream_k_vs_dp": sweep,
         }
         print(json.dumps(line), flush=True)
     if dist:

@@ -154,7 +154,14 @@ sk_status sk_predict_time(const sk_cost_params* params, const sk_tile_grid_t* gr
 /* argmin over g in {1..p} U {t} (costmodel.cpp:30-48); g == t is data-parallel. */
 sk_status sk_select_grid_size(const sk_cost_params* params, const sk_tile_grid_t* grid, int64_t p,
                               int64_t* g);
-/* Non-negative least squares over n >= 5 measured (grid, g, time) samples. */
+/* Predicted time of data_parallel, stream_k(param) or two_tile_sk_dp(param). */
+sk_status sk_predict_schedule(const sk_cost_params* params, const sk_tile_grid_t* grid,
+                              int32_t strategy, int64_t param, int64_t p, double* out);
+/* The Stream-K policy: argmin over data_parallel, stream_k(1..p) and
+ * two_tile_sk_dp(p); data-parallel unless another wins by > margin. */
+sk_status sk_select_schedule(const sk_cost_params* params, const sk_tile_grid_t* grid, int64_t p,
+                             int32_t* strategy, int64_t* param);
+/* Non-negative least squares over n >= 6 measured (grid, g, time) samples. */
 sk_status sk_calibrate(const sk_tile_grid_t* grids, const int64_t* g, const double* times,
                        int64_t n, int64_t p, sk_cost_params* out);
 

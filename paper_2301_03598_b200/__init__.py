@@ -113,6 +113,10 @@ _SIGS = {
     "sk_predict_time": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, _P(C.c_double)]),
     "sk_select_grid_size": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, _P(C.c_int64)]),
     "sk_calibrate": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_void_p]),
+    "sk_predict_schedule": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int64, C.c_int64,
+                                      _P(C.c_double)]),
+    "sk_select_schedule": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, _P(C.c_int32),
+                                     _P(C.c_int64)]),
 }
 
 
@@ -448,16 +452,25 @@ def calibrate(samples, p: int, margin: float = 0.15) -> CostParams:
     return out
 
 
+def predict_schedule(params: CostParams, grid: "TileGrid", strategy: "Strategy", param: int,
+                     p: int) -> float:
+    out = C.c_double()
+    _check(lib().sk_predict_schedule(C.byref(params), C.byref(grid._c()), int(strategy), param, p,
+                                     C.byref(out)), "predict_schedule")
+    return out.value
+
+
 def auto_stream_k(problem: "GemmProblem", blocking: "BlockingFactors", p: int,
                   params: Optional[CostParams] = None) -> "WorkAssignment":
-    """stream_k with the model-selected grid size (the paper's Stream-K policy);
-    g == t returns the equivalent data-parallel schedule (stream_k(t) == DP)."""
+    """The Stream-K policy (sk_select_schedule): the model's argmin over
+    data_parallel, stream_k(g <= p) and two_tile_sk_dp(p), keeping
+    data-parallel unless another schedule is predicted to win by > margin."""
     params = params or default_cost_params()
     grid = tile_grid(problem, blocking)
-    g = select_grid_size(params, grid, p)
-    if g == min(grid.total_tiles, grid.total_iters) and grid.total_tiles <= grid.total_iters:
-        return data_parallel(problem, blocking)
-    return stream_k(problem, blocking, g)
+    s, prm = C.c_int32(), C.c_int64()
+    _check(lib().sk_select_schedule(C.byref(params), C.byref(grid._c()), p, C.byref(s),
+                                    C.byref(prm)), "select_schedule")
+    return _assignment(Strategy(s.value), problem, blocking, prm.value)
 
 
 def corpus(seed: int = 0, count: int = 32824, lo: int = 128, hi: int = 8192) -> np.ndarray:

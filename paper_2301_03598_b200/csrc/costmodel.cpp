@@ -173,6 +173,74 @@ sk_status sk_select_grid_size(const sk_cost_params* c, const sk_tile_grid_t* g, 
   return SK_OK;
 }
 
+// Predicted time of a whole schedule: data_parallel, stream_k(g) or the
+// two-tile Stream-K + data-parallel hybrid (decompose.cpp:81-121), whose DP
+// waves run first and whose SK region is one balanced wave of p units.
+sk_status sk_predict_schedule(const sk_cost_params* c, const sk_tile_grid_t* g, int32_t strategy,
+                              int64_t param, int64_t p, double* out) {
+  if (!c || !valid_grid(g) || p < 1 || !out) return SK_EINVAL;
+  switch (strategy) {
+    case SK_DATA_PARALLEL:
+      return sk_predict_time(c, g, g->total_tiles, p, out);
+    case SK_STREAM_K:
+      return sk_predict_time(c, g, param, p, out);
+    case SK_TWO_TILE_SK_DP: {
+      if (param < 1) return SK_EINVAL;
+      const int64_t t = g->total_tiles, w = t / param, r = t % param;
+      if (r == 0) return sk_predict_time(c, g, t, p, out);
+      const int64_t d = w >= 2 ? (w - 1) * param : 0;
+      sk_tile_grid_t sk_region = *g;  // the trailing t - d tiles as one Stream-K problem
+      sk_region.total_tiles = t - d;
+      sk_region.total_iters = (t - d) * g->iters_per_tile;
+      double f[kF];
+      features(sk_region, param, p, f);
+      double t_sk = dot(*c, f);
+      const double dp_waves = static_cast<double>(cdiv(d, p));
+      *out = t_sk + dp_waves * (c->a + c->c * static_cast<double>(g->iters_per_tile) + c->s);
+      return SK_OK;
+    }
+    default:
+      return SK_EUNSUPPORTED;
+  }
+}
+
+// The Stream-K policy: argmin over data_parallel, stream_k(g) for g in 1..p and
+// two_tile_sk_dp(p), leaving data-parallel only for a predicted gain > margin.
+sk_status sk_select_schedule(const sk_cost_params* c, const sk_tile_grid_t* g, int64_t p,
+                             int32_t* strategy, int64_t* param) {
+  if (!c || !valid_grid(g) || p < 1 || !strategy || !param) return SK_EINVAL;
+  double t_dp;
+  sk_predict_schedule(c, g, SK_DATA_PARALLEL, 1, p, &t_dp);
+  int64_t gbest;
+  sk_cost_params nomargin = *c;
+  nomargin.margin = 0.0;
+  sk_select_grid_size(&nomargin, g, p, &gbest);
+  int32_t best_s = SK_STREAM_K;
+  int64_t best_p = gbest;
+  double bt;
+  sk_predict_time(c, g, gbest, p, &bt);
+  if (gbest == std::min(g->total_tiles, g->total_iters)) {
+    best_s = SK_DATA_PARALLEL;
+    best_p = 1;
+  }
+  if (g->total_tiles > p && g->total_tiles % p != 0) {
+    double t2;
+    sk_predict_schedule(c, g, SK_TWO_TILE_SK_DP, p, p, &t2);
+    if (t2 < bt) {
+      bt = t2;
+      best_s = SK_TWO_TILE_SK_DP;
+      best_p = p;
+    }
+  }
+  if (best_s != SK_DATA_PARALLEL && !(bt < (1.0 - c->margin) * t_dp)) {
+    best_s = SK_DATA_PARALLEL;
+    best_p = 1;
+  }
+  *strategy = best_s;
+  *param = best_p;
+  return SK_OK;
+}
+
 sk_status sk_calibrate(const sk_tile_grid_t* grids, const int64_t* gs, const double* times,
                        int64_t n, int64_t p, sk_cost_params* out) {
   if (!grids || !gs || !times || !out || n < kF || p < 1) return SK_EINVAL;
@@ -212,11 +280,11 @@ sk_status sk_default_cost_params(sk_dtype ab_type, sk_variant variant, sk_cost_p
   if (ab_type != SK_BFLOAT16 && ab_type != SK_FLOAT16 && ab_type != SK_FLOAT64) return SK_EINVAL;
   sk_cost_params c{};
   if (ab_type == SK_FLOAT64) {
-    c = {4.0, 0.5, 0.5, 0.02, 1.0, 1.0, 0.15, 0.0};
+    c = {4.0, 0.5, 0.5, 0.02, 1.0, 1.0, 0.2, 0.0};
   } else if (variant == SK_VARIANT_2SM || variant == SK_VARIANT_AUTO) {
-    c = {3.9049, 0.9955, 0.4063, 0.3098, 2.3291, 3.3913, 0.15, 0.0};
+    c = {3.9049, 0.9955, 0.4063, 0.3098, 2.3291, 3.3913, 0.2, 0.0};
   } else {
-    c = {3.9049, 0.9955, 0.4063, 0.1549, 2.3291, 3.3913, 0.15, 0.0};
+    c = {3.9049, 0.9955, 0.4063, 0.1549, 2.3291, 3.3913, 0.2, 0.0};
   }
   *out = c;
   return SK_OK;

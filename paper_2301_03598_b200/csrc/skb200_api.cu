@@ -31,6 +31,11 @@ uint32_t make_idesc_f16(bool bf16, int M, int N);
 size_t f16_slab_bytes();
 cudaError_t launch_f16(int cg, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
                        const KernelParams& p, int grid, cudaStream_t stream);
+// sk_gemm_f64.cu
+size_t f64_slab_bytes();
+cudaError_t f64_max_ctas_per_sm(int* out);
+cudaError_t launch_f64(const CUtensorMap& a, const CUtensorMap& b, double* C, int64_t ldc,
+                       const KernelParams& p, int grid, cudaStream_t stream);
 // sk_convert.cu
 cudaError_t launch_f32_to_16(const float* src, void* dst, int64_t rows, int64_t cols,
                              int64_t ld_dst, bool bf16, cudaStream_t stream);
@@ -203,6 +208,10 @@ sk_status pick_kernel(const sk_gemm_desc* d, Kernel* k) {
       return SK_OK;
     }
     return fail(SK_EINVAL, "unknown variant %d", d->variant);
+  }
+  if (d->ab_type == SK_FLOAT64) {
+    *k = Kernel::F64;
+    return SK_OK;
   }
   return fail(SK_EUNSUPPORTED, "ab_type %d has no device kernel", d->ab_type);
 }
@@ -477,6 +486,30 @@ sk_status sk_gemm(const sk_gemm_desc* d, void* ws, size_t ws_bytes, void* stream
       e = launch_f16(cg, ta, tb, tc, P, static_cast<int>(P.num_ctas), strm);
     }
     if (e != cudaSuccess) return cuda_fail(e, cg == 2 ? "sk_gemm_f16<2> launch" : "sk_gemm_f16<1> launch");
+    return SK_OK;
+  }
+  if (kern == Kernel::F64) {
+    CUtensorMap ta, tb;
+    st = make_tmap(&ta, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, d->A, d->problem.m, d->problem.k,
+                   d->lda, 16, 64, CU_TENSOR_MAP_SWIZZLE_128B);
+    if (st) return st;
+    st = make_tmap(&tb, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, d->B, d->problem.k, d->problem.n,
+                   d->ldb, 16, 16, CU_TENSOR_MAP_SWIZZLE_128B);
+    if (st) return st;
+    cudaError_t e;
+    {
+      std::lock_guard<std::mutex> lk(g_dev_mu);
+      static int occ = 0;  // co-resident CTAs per SM (persistent grid must fit in one wave)
+      if (occ == 0) {
+        e = f64_max_ctas_per_sm(&occ);
+        if (e != cudaSuccess) return cuda_fail(e, "sk_gemm_f64 occupancy");
+        if (occ < 1) return fail(SK_ECUDA, "sk_gemm_f64 does not fit on an SM");
+      }
+      const int64_t cap64 = d->num_ctas > 0 ? d->num_ctas : static_cast<int64_t>(info.sms) * occ;
+      P.num_ctas = std::min<int64_t>(units, std::min<int64_t>(cap64, static_cast<int64_t>(info.sms) * occ));
+      e = launch_f64(ta, tb, static_cast<double*>(d->C), d->ldc, P, static_cast<int>(P.num_ctas), strm);
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "sk_gemm_f64 launch");
     return SK_OK;
   }
   return fail(SK_EUNSUPPORTED, "kernel not available");

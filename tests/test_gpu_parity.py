@@ -210,3 +210,60 @@ def test_large_square_checksums(sk, torch_cuda, var):
         assert torch.equal(C.double().sum(1), rows)
         assert torch.equal(C.double().sum(0), cols)
         assert torch.equal(C[sample].double(), exact_rows)
+
+
+# ---------------------------------------------------------------- FP64 (config 4)
+EPS64 = float(np.finfo(np.float64).eps)
+
+
+@pytest.mark.parametrize("shape", [(64, 64, 16), (200, 150, 300), (129, 65, 33), (512, 384, 1024)])
+def test_fp64_int_bit_exact_all_strategies(sk, port, shape):
+    m, n, k = shape
+    blk = sk.kernel_blocking(sk.DType.Float64)
+    assert (blk.blk_m, blk.blk_n, blk.blk_k) == (64, 64, 16)
+    A, B = int_operands(port, m, n, k, 314)
+    want = port.execute("data_parallel", 1, A, B, 64, 64, 16).astype(np.float64)
+    for a in strategies(sk, sk.GemmProblem(m, n, k), blk, 148):
+        got = sk.execute(a, A.astype(np.float64), B.astype(np.float64), compute=sk.DType.Float64)
+        assert got.dtype == np.float64
+        assert np.array_equal(got, want), (sk.strategy_name(a.strategy), a.param)
+
+
+def test_fp64_within_reference_bound(sk, port):
+    """execute<double> semantics: |c - ref| <= 8 eps64 k max(|ref|, 1) against the
+    oracle's gemm_reference<double> on the same inputs (random_matrix<double>)."""
+    import oracle
+
+    m, n, k = 300, 260, 1000
+    blk = sk.kernel_blocking(sk.DType.Float64)
+    A = port.random_matrix(m, k, 81, "float64")
+    B = port.random_matrix(k, n, 82, "float64")
+    ref = port.gemm_reference(A, B, 64, 64, 16)
+    for a in strategies(sk, sk.GemmProblem(m, n, k), blk, 148):
+        got = sk.execute(a, A, B, compute=sk.DType.Float64)
+        ok, max_abs, max_rel = oracle.verify(got, ref, k, EPS64)
+        assert ok, (sk.strategy_name(a.strategy), max_abs, max_rel)
+
+
+def test_fp64_trace_and_determinism(sk, torch_cuda):
+    torch = torch_cuda
+    problem = sk.GemmProblem(1024, 1024, 4096)
+    blk = sk.kernel_blocking(sk.DType.Float64)
+    g = torch.Generator(device="cuda").manual_seed(3)
+    A = torch.rand(problem.m, problem.k, device="cuda", dtype=torch.float64, generator=g)
+    B = torch.rand(problem.k, problem.n, device="cuda", dtype=torch.float64, generator=g)
+    for a in (sk.stream_k(problem, blk, 148), sk.hybrid(problem, blk, 148, sk.HybridVariant.DpOneTileSk)):
+        gemm = sk.Gemm(a, sk.DType.Float64, trace=True)
+        C1 = torch.empty(problem.m, problem.n, device="cuda", dtype=torch.float64)
+        C2 = torch.empty_like(C1)
+        gemm.run(A, B, C1)
+        gemm.run(A, B, C2)
+        gemm.check()
+        assert torch.equal(C1, C2)
+        ref = A @ B
+        assert bool(((C1 - ref).abs() <= 8 * EPS64 * problem.k * ref.abs().clamp(min=1)).all())
+        T = a.grid.total_tiles
+        tiles = gemm.trace.cpu().numpy()[:4 * T].reshape(T, 4)
+        peers = sk.fixup_peers_of(a)
+        for x in range(T):
+            assert tiles[x, 0] == peers[x][0] and tiles[x, 1] == peers[x][-1]
