@@ -36,6 +36,10 @@ sys.path.insert(0, ROOT)
 
 STRATS = {"data_parallel": 0, "fixed_split": 1, "stream_k": 2, "dp_one_tile_sk": 3,
           "two_tile_sk_dp": 4}
+# BASELINE.json "metric"; `value` is the TFLOP/s half, `pct_of_peak` and
+# `stream_k_vs_dp` carry the other two.
+METRIC = ("GEMM TFLOP/s and % of B200 tensor peak; geomean speedup of Stream-K vs "
+          "data-parallel")
 
 
 def parse():
@@ -49,7 +53,7 @@ def parse():
     ap.add_argument("--m", type=int, default=8192)
     ap.add_argument("--n", type=int, default=8192)
     ap.add_argument("--k", type=int, default=8192)
-    ap.add_argument("--dtype", default="bf16", choices=["bf16", "fp16"])
+    ap.add_argument("--dtype", default="bf16", choices=["bf16", "fp16", "fp64"])
     ap.add_argument("--variant", default="2sm", choices=["auto", "1sm", "2sm"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -151,17 +155,19 @@ def cpu_reference_leg(args, strategy, param, blk, rows=None):
     kind = "reference" if oracle.have_reference() else "port"
     orc = oracle.Oracle(kind)
     threads = os.cpu_count() or 1
-    rows = rows or args.cpu_rows or 3072
+    fp64 = args.dtype == "fp64"
+    rows = rows or args.cpu_rows or (1536 if fp64 else 3072)
     m, n, k = rows, args.n, args.k
-    A = orc.random_matrix(m, k, 42, "float32")
-    B = orc.random_matrix(k, n, 43, "float32")
+    dt_name, tname = ("float64", "double") if fp64 else ("float32", "float")
+    A = orc.random_matrix(m, k, 42, dt_name)
+    B = orc.random_matrix(k, n, 43, dt_name)
     # same decomposition family on the sampled problem; the grid knob is the CPU's p
     prm = param if strategy != 1 else max(param, 1)
     t0 = time.perf_counter()
     orc.execute(strategy, prm, A, B, blk[0], blk[1], blk[2], threads=threads)
     dt = time.perf_counter() - t0
     tf = 2.0 * m * n * k / dt / 1e12
-    sample = (f"streamk::execute<float> ({kind}) {m}x{n}x{k} row sample of {args.m}x{args.n}x{args.k}, "
+    sample = (f"streamk::execute<{tname}> ({kind}) {m}x{n}x{k} row sample of {args.m}x{args.n}x{args.k}, "
               f"strategy {list(STRATS)[strategy]}, blk {blk[0]}x{blk[1]}x{blk[2]}")
     return tf, dt, sample, (threads if kind == "reference" else 1), kind
 
@@ -170,9 +176,14 @@ def run_reference_arm(args, rank, world):
     if rank != 0:
         return
     # same tile config and grid knob as our arm (kernel_blocking of the variant)
-    blk = (256, 256, 64) if args.variant == "2sm" else (128, 256, 64)
+    if args.dtype == "fp64":
+        blk, p_dev = (64, 64, 16), 296
+    elif args.variant == "2sm":
+        blk, p_dev = (256, 256, 64), 74
+    else:
+        blk, p_dev = (128, 256, 64), 148
     strategy = STRATS[args.strategy]
-    param = args.param or (2 if strategy == 1 else (74 if args.variant == "2sm" else 148))
+    param = args.param or (2 if strategy == 1 else p_dev)
     vals = []
     last = None
     for i in range(args.warmup + args.steps):
@@ -182,10 +193,11 @@ def run_reference_arm(args, rank, world):
         last = (sample, cores, kind)
     v = statistics.median(vals) if vals else 0.0
     line = {
-        "impl": "reference", "metric": "GEMM TFLOP/s (Stream-K)", "value": v, "unit": "TFLOP/s",
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "TFLOP/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic (reference random_matrix<float>)",
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64" if args.dtype == "fp64" else "f32",
+        "data": "synthetic (reference random_matrix<%s>)" % ("double" if args.dtype == "fp64" else "float"),
         "config": {"workload": f"{args.m}x{args.n}x{args.k} GEMM, {args.strategy}, CPU row sample"},
         "cpu_baseline": {"value": v, "unit": "TFLOP/s", "cores": last[1], "kind": last[2],
                          "sample": last[0]},
@@ -216,14 +228,16 @@ def main():
         dist_.init_process_group("nccl", device_id=torch.device("cuda", local))
         dist = dist_
 
-    ab = sk.DType.BFloat16 if args.dtype == "bf16" else sk.DType.Float16
-    tdt = torch.bfloat16 if args.dtype == "bf16" else torch.float16
+    ab = {"bf16": sk.DType.BFloat16, "fp16": sk.DType.Float16, "fp64": sk.DType.Float64}[args.dtype]
+    tdt = {"bf16": torch.bfloat16, "fp16": torch.float16, "fp64": torch.float64}[args.dtype]
+    cdt = torch.float64 if args.dtype == "fp64" else torch.float32
     variant = {"auto": sk.Variant.Auto, "1sm": sk.Variant.OneSM, "2sm": sk.Variant.TwoSM}[args.variant]
     blk = sk.kernel_blocking(ab, variant)
     sms = torch.cuda.get_device_properties(local).multi_processor_count
     strategy = sk.Strategy(STRATS[args.strategy])
-    ranks_per = 2 if blk.blk_m == 256 else 1
-    param = args.param or (2 if strategy == sk.Strategy.FixedSplit else sms // ranks_per)
+    # p = co-resident persistent CTAs: SM pairs (2-SM), SMs (1-SM), 2 per SM (FP64 DMMA)
+    p_dev = 2 * sms if args.dtype == "fp64" else sms // (2 if blk.blk_m == 256 else 1)
+    param = args.param or (2 if strategy == sk.Strategy.FixedSplit else p_dev)
     m, n, k = args.m, args.n, args.k  # this rank's column block: n columns of a N*n GEMM
     problem = sk.GemmProblem(m, n, k)
     a = sk._assignment(strategy, problem, blk, param)
@@ -232,7 +246,7 @@ def main():
     g = torch.Generator(device="cuda").manual_seed(1234 + rank)
     A = (torch.rand(m, k, device="cuda", generator=g) * 2 - 1).to(tdt)
     B = (torch.rand(k, n, device="cuda", generator=g) * 2 - 1).to(tdt)
-    Cout = torch.empty(m, n, device="cuda", dtype=torch.float32)
+    Cout = torch.empty(m, n, device="cuda", dtype=cdt)
     gemm = sk.Gemm(a, ab, variant)
     gemm_dp = sk.Gemm(a_dp, ab, variant)
     stream = torch.cuda.current_stream()
@@ -269,6 +283,10 @@ def main():
     value = flops * world / (ms * 1e-3) / 1e12  # whole-job TFLOP/s
     per_launch_tflops = flops / (ms * 1e-3) / 1e12
     peak_tf, _, peak_kind = load_peaks()
+    peak_kind = f"{peak_kind} bf16_tflops (burst)"
+    if args.dtype == "fp64":  # no measured FP64 peak in MEASURED_PEAKS.json: datasheet
+        peak_tf, peak_kind = 40.0, "datasheet B200 FP64 tensor (40 TFLOP/s)"
+    esz = A.element_size()
     workload = f"{m}x{n}x{k}_{args.dtype}_{sk.strategy_name(strategy)}_{blk.blk_m}x{blk.blk_n}x{blk.blk_k}"
 
     # ---- end to end through the reference-facing C-ABI call (sk_execute): pinned
@@ -277,9 +295,12 @@ def main():
     if not args.no_e2e:
         Ah = A.cpu().pin_memory()
         Bh = B.cpu().pin_memory()
-        Ch = torch.empty(m, n, dtype=torch.float32).pin_memory()
-        An = Ah.view(torch.int16).numpy().view(np.uint16 if ab == sk.DType.BFloat16 else np.float16)
-        Bn = Bh.view(torch.int16).numpy().view(np.uint16 if ab == sk.DType.BFloat16 else np.float16)
+        Ch = torch.empty(m, n, dtype=cdt).pin_memory()
+        if ab == sk.DType.Float64:
+            An, Bn = Ah.numpy(), Bh.numpy()
+        else:
+            An = Ah.view(torch.int16).numpy().view(np.uint16 if ab == sk.DType.BFloat16 else np.float16)
+            Bn = Bh.view(torch.int16).numpy().view(np.uint16 if ab == sk.DType.BFloat16 else np.float16)
         Cn = Ch.numpy()
         lib = sk.lib()
         pc, bc = problem._c(), blk._c()
@@ -305,7 +326,8 @@ def main():
             dt = float(t.item())
         e2e = {"value": flops * world / dt / 1e12, "unit": "TFLOP/s",
                "h2d_bytes_per_step": int(A.numel() * A.element_size() + B.numel() * B.element_size()),
-               "d2h_bytes_per_step": int(Cout.numel() * 4 + 4), "ms_per_step": dt * 1e3,
+               "d2h_bytes_per_step": int(Cout.numel() * Cout.element_size() + 4),
+               "ms_per_step": dt * 1e3,
                "path": "sk_execute (C ABI, host buffers, pinned)"}
         sk.lib().sk_execute_release()
 
@@ -316,9 +338,10 @@ def main():
     if rank == 0 and not args.no_sweep:
         from paper_2301_03598_b200 import sweep as sw
 
-        rows = sw.run(sw.CONFIG3, ["data_parallel", "stream_k:auto"], variant, args.dtype)
+        shapes, label = (sw.CONFIG4, "config4") if args.dtype == "fp64" else (sw.CONFIG3, "config3")
+        rows = sw.run(shapes, ["data_parallel", "stream_k:auto"], variant, args.dtype)
         summ = sw.summarise(rows)["stream_k:auto"]
-        sweep = {"shapes": "config3 (%d)" % len(sw.CONFIG3), "policy": "stream_k:auto (cost model)",
+        sweep = {"shapes": "%s (%d)" % (label, len(shapes)), "policy": "stream_k:auto (cost model)",
                  "geomean_sk_vs_dp": summ["geomean_speedup"], "min": summ["min"],
                  "max": summ["max"], "regress_gt_5pct": summ["regress_gt_5pct"]}
 
@@ -331,7 +354,7 @@ def main():
 
     if rank == 0:
         line = {
-            "metric": "GEMM TFLOP/s (Stream-K)", "value": value, "unit": "TFLOP/s",
+            "metric": METRIC, "value": value, "unit": "TFLOP/s",
             "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3),
             "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": args.dtype, "data": "synthetic uniform[-1,1) on device",
@@ -346,10 +369,11 @@ def main():
                               "speedup_sk_over_dp": ms_dp / ms},
             "roofline": {"bound": "tensor", "achieved": per_launch_tflops, "peak": peak_tf,
                          "unit": "TFLOP/s", "frac": per_launch_tflops / peak_tf,
-                         "peak_kind": f"{peak_kind} bf16_tflops (burst)",
+                         "peak_kind": peak_kind,
                          "traffic": load_traffic(workload),
                          "algorithmic": {"flops_per_launch": flops,
-                                         "bytes_per_launch": 2 * (m * k + k * n) + 4 * m * n}},
+                                         "bytes_per_launch": esz * (m * k + k * n)
+                                         + Cout.element_size() * m * n}},
             "clocks": clocks,
             "gpu_launches": args.steps,
             "e2e": e2e,

@@ -41,6 +41,11 @@ CONFIG3 = [
     (2560, 3840, 4096), (1024, 1024, 8192), (512, 512, 65536), (3072, 3072, 3072),
     (2304, 2304, 8192), (1280, 7680, 4096), (4096, 4096, 4096), (8192, 8192, 8192),
 ]
+# BASELINE config 4: FP64 squares 1024..8192 with the paper's 64x64x16 tile,
+# plus shapes whose 64x64 tile count sits just above a multiple of 296 CTAs.
+CONFIG4 = [(s, s, s) for s in (1024, 1536, 2048, 3072, 4096, 6144, 8192)] + [
+    (1216, 1024, 8192), (1088, 1152, 4096), (512, 512, 32768), (2432, 2048, 2048),
+]
 
 
 def strategies_for(problem, blk, p, names, params=None):
@@ -83,8 +88,11 @@ class ShapeTimer:
 
     def __init__(self, torch, m, n, k, tdt, max_copies=16, mem_budget=4 << 30):
         self.torch = torch
-        lda, ldb, ldc = -(-k // 8) * 8, -(-n // 8) * 8, -(-n // 4) * 4
-        foot = 2 * (m * lda + k * ldb)
+        es = torch.tensor([], dtype=tdt).element_size()
+        cdt = torch.float64 if tdt == torch.float64 else torch.float32
+        al = 16 // es  # 16-byte rows for TMA
+        lda, ldb, ldc = -(-k // al) * al, -(-n // al) * al, -(-n // 2) * 2 if es == 8 else -(-n // 4) * 4
+        foot = es * (m * lda + k * ldb)
         self.copies = int(max(1, min(max_copies, math.ceil(2 * L2_BYTES / foot),
                                      mem_budget // max(foot, 1))))
         self.cold = self.copies * foot > L2_BYTES
@@ -93,7 +101,7 @@ class ShapeTimer:
         self.B = [torch.empty(k, ldb, device="cuda", dtype=tdt)[:, :n] for _ in range(self.copies)]
         for t in self.A + self.B:
             t.copy_(torch.rand(t.shape, device="cuda", generator=g) * 2 - 1)
-        self.C = torch.empty(m, ldc, device="cuda", dtype=torch.float32)[:, :n]
+        self.C = torch.empty(m, ldc, device="cuda", dtype=cdt)[:, :n]
 
     def time_us(self, gemm, reps=3):
         torch = self.torch
@@ -123,11 +131,12 @@ class ShapeTimer:
 def run(shapes, names, variant, dtype, rank=0, world=1, log_every=0, params=None):
     import torch
 
-    ab = sk.DType.BFloat16 if dtype == "bf16" else sk.DType.Float16
-    tdt = torch.bfloat16 if dtype == "bf16" else torch.float16
+    ab = {"bf16": sk.DType.BFloat16, "fp16": sk.DType.Float16, "fp64": sk.DType.Float64}[dtype]
+    tdt = {"bf16": torch.bfloat16, "fp16": torch.float16, "fp64": torch.float64}[dtype]
     blk = sk.kernel_blocking(ab, variant)
     sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
-    p = sms // (2 if variant == sk.Variant.TwoSM else 1)
+    # p = co-resident persistent CTAs: pairs for 2-SM, 2 DMMA CTAs per SM for FP64
+    p = 2 * sms if dtype == "fp64" else sms // (2 if variant == sk.Variant.TwoSM else 1)
     params = params or sk.default_cost_params(ab, variant)
     rows = []
     for idx, (m, n, k) in enumerate(shapes):
@@ -142,7 +151,9 @@ def run(shapes, names, variant, dtype, rank=0, world=1, log_every=0, params=None
                          "iters_per_tile": a.grid.iters_per_tile,
                          "strategy": getattr(a, "label", sk.strategy_name(a.strategy)),
                          "param": a.param, "tiles_m": a.grid.tiles_m, "tiles_n": a.grid.tiles_n,
-                         "g": a.grid_size, "variant": "2sm" if variant == sk.Variant.TwoSM else "1sm",
+                         "g": a.grid_size,
+                         "variant": "dmma" if dtype == "fp64" else (
+                             "2sm" if variant == sk.Variant.TwoSM else "1sm"),
                          "dtype": dtype, "copies": timer.copies, "l2_cold": int(timer.cold),
                          "time_us": t, "tflops": 2.0 * m * n * k / (t * 1e-6) / 1e12})
         del timer
@@ -193,14 +204,14 @@ def write_csv(path, rows):
 
 def main(argv=None):
     ap = argparse.ArgumentParser()
-    ap.add_argument("--shapes", default="config3", choices=["config3", "corpus"])
+    ap.add_argument("--shapes", default="config3", choices=["config3", "config4", "corpus"])
     ap.add_argument("--count", type=int, default=32824)
     ap.add_argument("--offset", type=int, default=0)
     ap.add_argument("--lo", type=int, default=128)
     ap.add_argument("--hi", type=int, default=8192)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--variant", default="2sm", choices=["1sm", "2sm"])
-    ap.add_argument("--dtype", default="bf16", choices=["bf16", "fp16"])
+    ap.add_argument("--dtype", default="bf16", choices=["bf16", "fp16", "fp64"])
     ap.add_argument("--strategies", default="data_parallel,stream_k,two_tile_sk_dp,dp_one_tile_sk")
     ap.add_argument("--out", default="sweep.csv")
     ap.add_argument("--log-every", type=int, default=0)
@@ -215,6 +226,8 @@ def main(argv=None):
     torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
     if args.shapes == "config3":
         shapes = CONFIG3
+    elif args.shapes == "config4":
+        shapes = CONFIG4
     else:
         c = sk.corpus(args.seed, args.offset + args.count, args.lo, args.hi)[args.offset:]
         shapes = [tuple(int(x) for x in r[:3]) for r in c]
@@ -239,8 +252,8 @@ def main(argv=None):
         summary = {"sweep": args.shapes, "variant": args.variant, "dtype": args.dtype,
                    "world": world, **summarise(allrows)}
         if args.calibrate:
-            p = torch.cuda.get_device_properties(0).multi_processor_count // (
-                2 if args.variant == "2sm" else 1)
+            sms = torch.cuda.get_device_properties(0).multi_processor_count
+            p = 2 * sms if args.dtype == "fp64" else sms // (2 if args.variant == "2sm" else 1)
             params, n = fit_cost_model(allrows, p)
             summary["cost_params"] = params.as_dict()
             summary["calibration_samples"] = n
