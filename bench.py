@@ -277,6 +277,15 @@ def main():
         ms = timed(gemm, args.steps, max(args.warmup, 3))
     gemm.check()
     clocks = clk.summary()
+    # Cross-check with the clock the kernel itself sees: clock64 / globaltimer
+    # stamped by every CTA of a traced launch run back-to-back after the timed
+    # region (same power state).
+    traced = sk.Gemm(a, ab, variant, trace=True)
+    for _ in range(max(3, min(args.steps, 10))):
+        traced.run(A, B, Cout)
+    torch.cuda.synchronize()
+    clocks["kernel_sm_mhz"] = traced.clock_mhz()
+    del traced
     ms_dp = timed(gemm_dp, max(args.steps // 2, 3), 3)
     gemm_dp.check()
 

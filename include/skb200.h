@@ -107,6 +107,8 @@ typedef struct sk_gemm_desc {
   void* C;              /* FLOAT32 for BF16/FP16 inputs, FLOAT64 for FP64 */
   int64_t ldc;          /* >= n, ldc * sizeof(c) % 16 == 0 */
   int32_t* trace;       /* optional device buffer, see sk_trace_size(); NULL = off */
+  int64_t* cta_clocks;  /* optional device buffer of 4 * grid int64: per launched CTA
+                           {clock64 start, globaltimer ns start, clock64 end, globaltimer end} */
 } sk_gemm_desc;
 
 const char* sk_status_string(sk_status status);

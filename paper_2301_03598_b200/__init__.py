@@ -81,7 +81,7 @@ class sk_gemm_desc(C.Structure):
         ("ab_type", C.c_int32), ("param", C.c_int64), ("variant", C.c_int32),
         ("num_ctas", C.c_int32), ("A", C.c_void_p), ("lda", C.c_int64), ("B", C.c_void_p),
         ("ldb", C.c_int64), ("C", C.c_void_p), ("ldc", C.c_int64),
-        ("trace", C.c_void_p),
+        ("trace", C.c_void_p), ("cta_clocks", C.c_void_p),
     ]
 
 
@@ -565,6 +565,15 @@ class Gemm:
             _check(lib().sk_trace_size(C.byref(d), C.byref(n)), "trace_size")
             self.trace = torch.full((n.value,), -1, dtype=torch.int32, device="cuda")
             self.trace[4 * a.grid.total_tiles:] = 0
+        # per-CTA {clock64, globaltimer} stamps at start/end (clock_mhz())
+        self.cta_clocks = torch.zeros(4 * 2 * 512, dtype=torch.int64, device="cuda") if trace else None
+
+    def clock_mhz(self) -> float:
+        """Effective SM clock of the last traced launch: median over CTAs of
+        d(clock64) / d(globaltimer)."""
+        c = self.cta_clocks.view(-1, 4).cpu().numpy()
+        c = c[(c[:, 3] > c[:, 1]) & (c[:, 2] > c[:, 0])]
+        return float(np.median((c[:, 2] - c[:, 0]) / (c[:, 3] - c[:, 1]) * 1e3)) if len(c) else 0.0
 
     def run(self, A, B, Cout, stream=None) -> None:
         import torch
@@ -577,6 +586,7 @@ class Gemm:
         d.B, d.ldb = B.data_ptr(), B.stride(0)
         d.C, d.ldc = Cout.data_ptr(), Cout.stride(0)
         d.trace = self.trace.data_ptr() if self.trace is not None else None
+        d.cta_clocks = self.cta_clocks.data_ptr() if self.cta_clocks is not None else None
         s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
         _check(lib().sk_gemm(C.byref(d), C.c_void_p(self.workspace.data_ptr()), self.ws_bytes,
                              C.c_void_p(s)), "sk_gemm")

@@ -164,6 +164,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   // kernel's tail; nothing below touches global memory before it completes.
   ptx::grid_dependency_wait();
   ptx::launch_dependents();
+  stamp_clock(P, 0);
 
   if (warp == 0) {
     // ===================== TMA producer (every CTA of the pair) =====================
@@ -369,6 +370,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if constexpr (CG == 2) cluster_sync();  // the leader's MMAs touch the peer's smem/TMEM
   ptx::tc_fence_after();
   if (warp == 1) ptx::tmem_dealloc<CG>(tmem_base, TMEM_COLS);
+  stamp_clock(P, 1);
 #endif
 }
 

@@ -39,6 +39,7 @@ struct KernelParams {
   int* flags;
   int* err;
   int* trace;
+  long long* cta_clocks;  // optional: per CTA {clock64, globaltimer} at start and end
   int64_t watchdog_ns;
   int64_t raster_rows;  // data-parallel tile-row group height (1 = row-major)
 };
@@ -107,6 +108,16 @@ __device__ __forceinline__ void for_each_segment(const Schedule& s, int64_t cta,
   } else {  // StreamK, DpOneTileSk: SK ids above the DP ids
     desc_phase(s.bal.first_id, s.bal.first_id + s.bal.count);
     dp_phase();
+  }
+}
+
+// Per-CTA clock stamps (sk_gemm_desc.cta_clocks): the effective SM clock of a
+// launch is (clock64 end - start) / (globaltimer end - start).
+__device__ __forceinline__ void stamp_clock(const KernelParams& P, int slot) {
+  if (P.cta_clocks && threadIdx.x == 0) {
+    long long* c = P.cta_clocks + 4 * blockIdx.x + 2 * slot;
+    c[0] = static_cast<long long>(clock64());
+    c[1] = static_cast<long long>(ptx::globaltimer());
   }
 }
 

@@ -458,6 +458,7 @@ sk_status sk_gemm(const sk_gemm_desc* d, void* ws, size_t ws_bytes, void* stream
   P.flags = reinterpret_cast<int*>(wsb + L.flags_off);
   P.partials = wsb + L.partials_off;
   P.trace = d->trace;
+  P.cta_clocks = reinterpret_cast<long long*>(d->cta_clocks);
   P.watchdog_ns = 4000000000LL;
   P.raster_rows = 16;
   if (const char* e = getenv("SKB200_RASTER_ROWS")) P.raster_rows = std::max(1, atoi(e));
