@@ -69,7 +69,7 @@ typedef enum sk_dtype {
 
 /* Kernel family: one tile configuration per precision. */
 typedef enum sk_variant {
-  SK_VARIANT_AUTO = 0,
+  SK_VARIANT_AUTO = 0, /* the kernel whose tile equals the blocking; 2-SM by default */
   SK_VARIANT_1SM = 1, /* BF16/FP16: 128x256x64, tcgen05 cta_group::1, persistent grid = #SMs */
   SK_VARIANT_2SM = 2  /* BF16/FP16: 256x256x64, tcgen05 cta_group::2, persistent grid = #SMs/2 pairs */
 } sk_variant;

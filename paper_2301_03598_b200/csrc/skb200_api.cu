@@ -199,11 +199,14 @@ enum class Kernel { F16_1SM, F16_2SM, F64 };
 
 sk_status pick_kernel(const sk_gemm_desc* d, Kernel* k) {
   if (d->ab_type == SK_BFLOAT16 || d->ab_type == SK_FLOAT16) {
-    if (d->variant == SK_VARIANT_AUTO || d->variant == SK_VARIANT_1SM) {
+    // AUTO: the blocking names the kernel (128x256x64 -> 1-SM); default 2-SM.
+    if (d->variant == SK_VARIANT_1SM ||
+        (d->variant == SK_VARIANT_AUTO && d->blocking.blk_m == 128 && d->blocking.blk_n == 256 &&
+         d->blocking.blk_k == 64)) {
       *k = Kernel::F16_1SM;
       return SK_OK;
     }
-    if (d->variant == SK_VARIANT_2SM) {
+    if (d->variant == SK_VARIANT_2SM || d->variant == SK_VARIANT_AUTO) {
       *k = Kernel::F16_2SM;
       return SK_OK;
     }

@@ -57,10 +57,16 @@ def test_status_strings_and_version(sk):
 
 
 def test_kernel_blocking_per_precision(sk):
-    b = sk.kernel_blocking(sk.DType.BFloat16)
-    assert (b.blk_m, b.blk_n, b.blk_k) == (128, 256, 64)
+    b = sk.kernel_blocking(sk.DType.BFloat16)  # AUTO -> 2-SM
+    assert (b.blk_m, b.blk_n, b.blk_k) == (256, 256, 64)
     b = sk.kernel_blocking(sk.DType.Float16, sk.Variant.OneSM)
     assert (b.blk_m, b.blk_n, b.blk_k) == (128, 256, 64)
+    b = sk.kernel_blocking(sk.DType.Float64)
+    assert (b.blk_m, b.blk_n, b.blk_k) == (64, 64, 16)
+    # AUTO with an explicit 1-SM blocking resolves to the 1-SM kernel
+    d = _desc(sk, 512, 512, 512, (128, 256, 64), strategy=0, param=1)
+    n = C.c_size_t()
+    assert sk.lib().sk_workspace_size(C.byref(d), C.byref(n)) == 0
 
 
 def _desc(sk, m, n, k, blk, strategy=2, param=148, ab=3):

@@ -267,3 +267,75 @@ def test_fp64_trace_and_determinism(sk, torch_cuda):
         peers = sk.fixup_peers_of(a)
         for x in range(T):
             assert tiles[x, 0] == peers[x][0] and tiles[x, 1] == peers[x][-1]
+
+
+def test_double_signal_raises_protocol_error_and_recovers(sk, torch_cuda):
+    """FixupStore::signal's double-signal check (executor.hpp:108-112, :203-205):
+    a flag found already set when a non-owner signals is a protocol violation
+    -> ProtocolError (std::logic_error); the next launch on the same workspace
+    is clean again."""
+    torch = torch_cuda
+    problem = sk.GemmProblem(512, 512, 2048)
+    blk = sk.kernel_blocking(sk.DType.BFloat16, sk.Variant.OneSM)
+    a = sk.stream_k(problem, blk, 37)
+    gemm = sk.Gemm(a, sk.DType.BFloat16, sk.Variant.OneSM)
+    A = torch.ones(problem.m, problem.k, dtype=torch.bfloat16, device="cuda")
+    B = torch.ones(problem.k, problem.n, dtype=torch.bfloat16, device="cuda")
+    C = torch.empty(problem.m, problem.n, device="cuda")
+    gemm.run(A, B, C)
+    gemm.check()
+    assert torch.equal(C, torch.full_like(C, 2048.0))
+    # corrupt: pre-set every flag (the --corrupt idea of tools/streamk_main.cpp:129)
+    gemm.workspace[256:256 + 4 * 37].view(torch.int32).fill_(1)
+    gemm.run(A, B, C)
+    with pytest.raises(sk.ProtocolError):
+        gemm.check()
+    gemm.run(A, B, C)  # dirty flags are cleared before the next launch
+    gemm.check()
+    assert torch.equal(C, torch.full_like(C, 2048.0))
+
+
+def test_pitched_views_and_alignment(sk, torch_cuda):
+    """Leading dimensions larger than the row (pitched views) are honoured;
+    misaligned leading dimensions are rejected (SK_EUNSUPPORTED) before launch."""
+    torch = torch_cuda
+    m, n, k = 300, 520, 700
+    blk = sk.kernel_blocking()
+    Abig = torch.randint(-8, 8, (m, 1024), device="cuda").to(torch.bfloat16)
+    Bbig = torch.randint(-8, 8, (k, 768), device="cuda").to(torch.bfloat16)
+    Cbig = torch.zeros(m, 640, device="cuda")
+    A, B, Cv = Abig[:, :k], Bbig[:, :n], Cbig[:, :n]
+    gemm = sk.Gemm(sk.stream_k(sk.GemmProblem(m, n, k), blk, 11))
+    gemm.run(A, B, Cv)
+    gemm.check()
+    assert torch.equal(Cv, (A.double() @ B.double()).float())
+    assert torch.equal(Cbig[:, n:], torch.zeros_like(Cbig[:, n:]))  # nothing written past n
+    bad = torch.zeros(m, k + 1, device="cuda", dtype=torch.bfloat16)[:, :k]  # ld = 701: not 16-B
+    with pytest.raises(sk.UnsupportedError):
+        gemm.run(bad, B, Cv)
+
+
+def test_graph_capture(sk, torch_cuda):
+    """sk_gemm is stream-ordered and capturable: a CUDA graph of launches
+    replays to the same result."""
+    torch = torch_cuda
+    m = n = 1024
+    k = 4096
+    blk = sk.kernel_blocking(sk.DType.BFloat16, sk.Variant.TwoSM)
+    gemm = sk.Gemm(sk.auto_stream_k(sk.GemmProblem(m, n, k), blk, 74), variant=sk.Variant.TwoSM)
+    A = torch.randint(-4, 4, (m, k), device="cuda").to(torch.bfloat16)
+    B = torch.randint(-4, 4, (k, n), device="cuda").to(torch.bfloat16)
+    C = torch.zeros(m, n, device="cuda")
+    gemm.run(A, B, C)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            gemm.run(A, B, C)
+    C.zero_()
+    g.replay()
+    g.replay()
+    torch.cuda.synchronize()
+    gemm.check()
+    assert torch.equal(C, (A.double() @ B.double()).float())
