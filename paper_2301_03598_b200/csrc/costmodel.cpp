@@ -280,7 +280,7 @@ sk_status sk_default_cost_params(sk_dtype ab_type, sk_variant variant, sk_cost_p
   if (ab_type != SK_BFLOAT16 && ab_type != SK_FLOAT16 && ab_type != SK_FLOAT64) return SK_EINVAL;
   sk_cost_params c{};
   if (ab_type == SK_FLOAT64) {
-    c = {0.0, 5.2158, 0.0, 0.71323, 0.95141, 0.62478, 0.2, 0.0};  // costmodel_fp64.json
+    c = {0.0, 5.2158, 0.0, 0.71323, 0.95141, 0.62478, 0.3, 0.0};  // costmodel_fp64.json
   } else if (variant == SK_VARIANT_2SM || variant == SK_VARIANT_AUTO) {
     c = {3.9049, 0.9955, 0.4063, 0.3098, 2.3291, 3.3913, 0.2, 0.0};
   } else {
