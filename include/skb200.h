@@ -47,7 +47,8 @@ typedef enum sk_status {
   SK_ECUDA = 3,         /* CUDA runtime / driver error; see sk_last_error() */
   SK_EPROTOCOL = 4,     /* fixup protocol violation: double signal or wait watchdog */
   SK_ERANGE = 5,        /* std::out_of_range (iter_to_coords) */
-  SK_ECAPACITY = 6      /* caller buffer too small; the required size is still reported */
+  SK_ECAPACITY = 6,     /* caller buffer too small; the required size is still reported */
+  SK_EIO = 7            /* std::runtime_error of the SKMX reader/writer; see sk_io_error() */
 } sk_status;
 
 /* Strategy tags: types.hpp:70 Strategy / decompose.hpp:9 HybridVariant. */
@@ -138,6 +139,15 @@ sk_status sk_quantization_efficiency(int64_t t, int64_t p, double* out);
  * {m, n, k, matrix_seed} of sample i, dims = clamp(llround(exp(ln lo + u (ln hi -
  * ln lo))), lo, hi) with u from SplitMix64(seed); matrix_seed = next(). */
 sk_status sk_corpus(uint64_t seed, int64_t count, int64_t lo, int64_t hi, uint64_t* out);
+
+/* ---- SKMX matrix files (matrix.hpp:70-93, matrix.cpp:13-61) --------------- */
+/* 16-byte LE header "SKMX", u32 dtype tag, u32 rows, u32 cols; row-major payload. */
+sk_status sk_save_matrix(const char* path, sk_dtype dtype, int64_t rows, int64_t cols,
+                         const void* data);
+sk_status sk_load_matrix_header(const char* path, sk_dtype* dtype, int64_t* rows, int64_t* cols);
+/* dtype tag must equal `expect` (else SK_EIO, the reference's runtime_error). */
+sk_status sk_load_matrix(const char* path, sk_dtype expect, int64_t rows, int64_t cols, void* data);
+const char* sk_io_error(void);
 
 /* ---- grid-size model (costmodel.hpp:13-60, wave-aware) -------------------- */
 /* time(g) = e + ceil(g/p) * (a + b*[peers>1] + c*ipc + d*(peers-1) + s*segs), microseconds;

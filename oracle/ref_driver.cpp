@@ -14,6 +14,7 @@
 // out_of_range=5, other=7).
 #include <cstdint>
 #include <cstring>
+#include <fstream>
 #include <sstream>
 #include <stdexcept>
 #include <string>
@@ -217,6 +218,37 @@ int ref_execute_i64(int strategy, int64_t param, int64_t m, int64_t n, int64_t k
                     int64_t bn, int64_t bk, const int64_t* A, const int64_t* B, int64_t* C,
                     int threads) {
   return execute_strategy(strategy, param, m, n, k, bm, bn, bk, A, B, C, threads);
+}
+
+// SKMX files through the reference's own save_matrix/load_matrix (matrix.hpp:78-93).
+int ref_save_matrix_f32(const char* path, int64_t r, int64_t c, const float* data) {
+  return guarded([&] {
+    std::ofstream out(path, std::ios::binary);
+    save_matrix(wrap(data, r, c), out);
+  });
+}
+int ref_save_matrix_f64(const char* path, int64_t r, int64_t c, const double* data) {
+  return guarded([&] {
+    std::ofstream out(path, std::ios::binary);
+    save_matrix(wrap(data, r, c), out);
+  });
+}
+int ref_save_matrix_i64(const char* path, int64_t r, int64_t c, const int64_t* data) {
+  return guarded([&] {
+    std::ofstream out(path, std::ios::binary);
+    save_matrix(wrap(data, r, c), out);
+  });
+}
+// Loads a float32 SKMX file; returns 7 (runtime_error) on bad magic / dtype.
+int ref_load_matrix_f32(const char* path, int64_t* r, int64_t* c, float* data, int64_t cap) {
+  return guarded([&] {
+    std::ifstream in(path, std::ios::binary);
+    const Matrix<float> m = load_matrix<float>(in);
+    *r = m.rows;
+    *c = m.cols;
+    if (data && cap >= m.rows * m.cols)
+      std::memcpy(data, m.data.data(), sizeof(float) * m.data.size());
+  });
 }
 
 // Corpus dims in run_sweep order (sweep.cpp:79-86), parsed from its CSV with

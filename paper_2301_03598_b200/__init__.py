@@ -117,6 +117,10 @@ _SIGS = {
                                       _P(C.c_double)]),
     "sk_select_schedule": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, _P(C.c_int32),
                                      _P(C.c_int64)]),
+    "sk_save_matrix": (C.c_int, [C.c_char_p, C.c_int, C.c_int64, C.c_int64, C.c_void_p]),
+    "sk_load_matrix_header": (C.c_int, [C.c_char_p, _P(C.c_int), _P(C.c_int64), _P(C.c_int64)]),
+    "sk_load_matrix": (C.c_int, [C.c_char_p, C.c_int, C.c_int64, C.c_int64, C.c_void_p]),
+    "sk_io_error": (C.c_char_p, []),
 }
 
 
@@ -471,6 +475,42 @@ def auto_stream_k(problem: "GemmProblem", blocking: "BlockingFactors", p: int,
     _check(lib().sk_select_schedule(C.byref(params), C.byref(grid._c()), p, C.byref(s),
                                     C.byref(prm)), "select_schedule")
     return _assignment(Strategy(s.value), problem, blocking, prm.value)
+
+
+class MatrixFileError(RuntimeError):
+    """std::runtime_error of the reference's SKMX reader (matrix.cpp:37-61)."""
+
+
+_NP_OF = {DType.Int64: np.int64, DType.Float32: np.float32, DType.Float64: np.float64,
+          DType.BFloat16: np.uint16, DType.Float16: np.float16}
+
+
+def save_matrix(path: str, a: np.ndarray, dtype: Optional[DType] = None) -> None:
+    """SKMX writer (matrix.hpp:78-84); uint16 arrays are stored as bfloat16."""
+    if dtype is None:
+        dtype = {np.dtype(v): k for k, v in _NP_OF.items()}[a.dtype]
+    a = np.ascontiguousarray(a, dtype=_NP_OF[dtype])
+    rows, cols = a.shape
+    st = lib().sk_save_matrix(os.fsencode(path), int(dtype), rows, cols, a.ctypes.data_as(C.c_void_p))
+    if st == 7:
+        raise MatrixFileError(lib().sk_io_error().decode())
+    _check(st, "save_matrix")
+
+
+def load_matrix(path: str, dtype: DType) -> np.ndarray:
+    """SKMX reader (matrix.hpp:86-93): the file's dtype tag must equal `dtype`."""
+    t, r, c = C.c_int(), C.c_int64(), C.c_int64()
+    st = lib().sk_load_matrix_header(os.fsencode(path), C.byref(t), C.byref(r), C.byref(c))
+    if st == 7:
+        raise MatrixFileError(lib().sk_io_error().decode())
+    _check(st, "load_matrix")
+    out = np.empty((r.value, c.value), _NP_OF[DType(dtype)])
+    st = lib().sk_load_matrix(os.fsencode(path), int(dtype), r.value, c.value,
+                              out.ctypes.data_as(C.c_void_p))
+    if st == 7:
+        raise MatrixFileError(lib().sk_io_error().decode())
+    _check(st, "load_matrix")
+    return out
 
 
 def corpus(seed: int = 0, count: int = 32824, lo: int = 128, hi: int = 8192) -> np.ndarray:

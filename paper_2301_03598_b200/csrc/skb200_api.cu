@@ -275,6 +275,7 @@ const char* sk_status_string(sk_status s) {
     case SK_EPROTOCOL: return "SK_EPROTOCOL: fixup protocol violation";
     case SK_ERANGE: return "SK_ERANGE: index out of range";
     case SK_ECAPACITY: return "SK_ECAPACITY: output buffer too small";
+    case SK_EIO: return "SK_EIO: matrix file error";
   }
   return "unknown sk_status";
 }

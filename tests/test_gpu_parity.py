@@ -339,3 +339,27 @@ def test_graph_capture(sk, torch_cuda):
     torch.cuda.synchronize()
     gemm.check()
     assert torch.equal(C, (A.double() @ B.double()).float())
+
+
+@pytest.mark.parametrize("var", ["1sm", "2sm", "fp64"])
+def test_random_instances_bit_exact(sk, port, var):
+    """acceptance.cpp criterion 4 on the device: seeded random problems (dims up to
+    700, every decomposition with random knobs) with integer-valued operands are
+    bit-exact against the oracle's int64 executor."""
+    rng = np.random.default_rng({"1sm": 11, "2sm": 22, "fp64": 33}[var])
+    if var == "fp64":
+        ab, V, dt = sk.DType.Float64, sk.Variant.Auto, np.float64
+    else:
+        ab, V, dt = sk.DType.BFloat16, variant(sk, var), np.float32
+    blk = sk.kernel_blocking(ab, V)
+    for trial in range(25):
+        m, n, k = (int(x) for x in rng.integers(1, 700, 3))
+        A, B = int_operands(port, m, n, k, int(rng.integers(1 << 40)))
+        want = (A.astype(np.float64) @ B.astype(np.float64)).astype(dt)
+        P = sk.GemmProblem(m, n, k)
+        for a in (sk.data_parallel(P, blk), sk.fixed_split(P, blk, int(rng.integers(1, 6))),
+                  sk.stream_k(P, blk, int(rng.integers(1, 300))),
+                  sk.hybrid(P, blk, int(rng.integers(1, 160)), sk.HybridVariant.DpOneTileSk),
+                  sk.hybrid(P, blk, int(rng.integers(1, 160)), sk.HybridVariant.TwoTileSkDp)):
+            got = sk.execute(a, A.astype(dt), B.astype(dt), compute=ab, variant=V)
+            assert np.array_equal(got, want), (trial, m, n, k, sk.strategy_name(a.strategy), a.param)
