@@ -110,6 +110,9 @@ typedef struct sk_gemm_desc {
   int32_t* trace;       /* optional device buffer, see sk_trace_size(); NULL = off */
   int64_t* cta_clocks;  /* optional device buffer of 4 * grid int64: per launched CTA
                            {clock64 start, globaltimer ns start, clock64 end, globaltimer end} */
+  int64_t* events;      /* optional device timeline, 8 int64 per record, see sk_timeline_size:
+                           {unit, tile, core, kind, t_mac_start, t_mac_end, t_wait_end, t_done},
+                           kind = 1 partial | 2 owner with peers | npeer << 8; ns */
 } sk_gemm_desc;
 
 const char* sk_status_string(sk_status status);
@@ -190,6 +193,9 @@ sk_status sk_workspace_check(void* workspace, void* stream);
 /* Ints needed for the optional ownership trace: per tile {owner, last_peer,
  * storing_unit, segments} followed by per unit {partials_emitted}. */
 sk_status sk_trace_size(const sk_gemm_desc* desc, int64_t* ints);
+/* Records of the optional device timeline: grid_size * seg_stride (record of
+ * unit u's i-th tile segment at u * seg_stride + i; unused records stay zero). */
+sk_status sk_timeline_size(const sk_gemm_desc* desc, int64_t* records, int64_t* seg_stride);
 /* Stream-ordered, asynchronous.  Does not synchronise. */
 sk_status sk_gemm(const sk_gemm_desc* desc, void* workspace, size_t workspace_bytes,
                   void* stream);

@@ -81,7 +81,7 @@ class sk_gemm_desc(C.Structure):
         ("ab_type", C.c_int32), ("param", C.c_int64), ("variant", C.c_int32),
         ("num_ctas", C.c_int32), ("A", C.c_void_p), ("lda", C.c_int64), ("B", C.c_void_p),
         ("ldb", C.c_int64), ("C", C.c_void_p), ("ldc", C.c_int64),
-        ("trace", C.c_void_p), ("cta_clocks", C.c_void_p),
+        ("trace", C.c_void_p), ("cta_clocks", C.c_void_p), ("events", C.c_void_p),
     ]
 
 
@@ -104,6 +104,7 @@ _SIGS = {
     "sk_workspace_init": (C.c_int, [C.c_void_p, C.c_size_t, C.c_void_p]),
     "sk_workspace_check": (C.c_int, [C.c_void_p, C.c_void_p]),
     "sk_trace_size": (C.c_int, [_P(sk_gemm_desc), _P(C.c_int64)]),
+    "sk_timeline_size": (C.c_int, [_P(sk_gemm_desc), _P(C.c_int64), _P(C.c_int64)]),
     "sk_gemm": (C.c_int, [_P(sk_gemm_desc), C.c_void_p, C.c_size_t, C.c_void_p]),
     "sk_execute": (C.c_int, [_P(sk_problem), _P(sk_blocking), C.c_int, C.c_int64, C.c_int, C.c_int,
                              C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32]),
@@ -575,7 +576,8 @@ class Gemm:
     """
 
     def __init__(self, a: WorkAssignment, ab_type: DType = DType.BFloat16,
-                 variant: Variant = Variant.Auto, num_ctas: int = 0, trace: bool = False):
+                 variant: Variant = Variant.Auto, num_ctas: int = 0, trace: bool = False,
+                 timeline: bool = False):
         import torch  # device memory only
 
         if a.param == 0:
@@ -607,6 +609,18 @@ class Gemm:
             self.trace[4 * a.grid.total_tiles:] = 0
         # per-CTA {clock64, globaltimer} stamps at start/end (clock_mhz())
         self.cta_clocks = torch.zeros(4 * 2 * 512, dtype=torch.int64, device="cuda") if trace else None
+        self.events = None
+        if timeline:
+            n, stride = C.c_int64(), C.c_int64()
+            _check(lib().sk_timeline_size(C.byref(d), C.byref(n), C.byref(stride)), "timeline_size")
+            self.events = torch.zeros(8 * max(n.value, 1), dtype=torch.int64, device="cuda")
+
+    def timeline(self) -> np.ndarray:
+        """Device-measured events of the last launch (timeline=True), one row per
+        tile segment: [unit, tile, core, kind, t_mac_start, t_mac_end, t_wait_end,
+        t_done] (globaltimer ns); see paper_2301_03598_b200.timeline."""
+        ev = self.events.view(-1, 8).cpu().numpy()
+        return ev[ev[:, 7] > 0]
 
     def clock_mhz(self) -> float:
         """Effective SM clock of the last traced launch: median over CTAs of
@@ -627,6 +641,7 @@ class Gemm:
         d.C, d.ldc = Cout.data_ptr(), Cout.stride(0)
         d.trace = self.trace.data_ptr() if self.trace is not None else None
         d.cta_clocks = self.cta_clocks.data_ptr() if self.cta_clocks is not None else None
+        d.events = self.events.data_ptr() if self.events is not None else None
         s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
         _check(lib().sk_gemm(C.byref(d), C.c_void_p(self.workspace.data_ptr()), self.ws_bytes,
                              C.c_void_p(s)), "sk_gemm")

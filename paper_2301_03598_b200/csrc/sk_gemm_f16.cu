@@ -208,9 +208,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     if (lane == 0 && leader_cta) {
       uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
       for_each_segment(s, cta, P.num_ctas, P.raster_rows,
-                       [&](int64_t, int64_t, int64_t lb, int64_t le) {
+                       [&](int64_t u, int64_t tile, int64_t lb, int64_t le) {
         ptx::mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         ptx::tc_fence_after();
+        if (long long* ev = event_slot(P, u, tile)) ev[kEvMacStart] = ptx::globaltimer();
         const uint32_t d_tmem = tmem_base + acc * BN;
         for (int64_t kb = lb; kb < le; ++kb) {
           ptx::mbar_wait(&full_bar[stage], phase);
@@ -256,6 +257,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                      [&](int64_t u, int64_t tile, int64_t lb, int64_t le) {
       ptx::mbar_wait(&tfull_bar[acc], acc_phase);
       ptx::tc_fence_after();
+      long long* ev = (leader && rank == 0) ? event_slot(P, u, tile) : nullptr;
+      if (ev) ev[kEvMacEnd] = ptx::globaltimer();
       const uint32_t tsrc = tmem_base + acc * BN + ((q * 32) << 16);
       const int32_t m0 = static_cast<int32_t>((tile / s.tiles_n) * (ROWS * CG) + rank * ROWS);
       const int32_t n0 = static_cast<int32_t>((tile % s.tiles_n) * BN);
@@ -268,6 +271,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           for (int p = 1; p <= npeer; ++p) wait_flag(P, P.flags + fidx(u + p));
         __syncwarp();
       }
+      if (ev) ev[kEvWaitEnd] = ptx::globaltimer();
       float* my_slab = partial ? partials + fidx(u) * static_cast<int64_t>(SLAB_ELEMS) : nullptr;
       // 64 columns (two 32-column chunks) per step: one tcgen05.ld.x64, 16 float4
       // of peer slab in flight per thread, two 32x32 TMA-store boxes.
@@ -357,6 +361,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           t[2] = static_cast<int>(u);
           t[3] = npeer;
         }
+      }
+      if (ev) {
+        ev[kEvUnit] = u;
+        ev[kEvTile] = tile;
+        ev[kEvCore] = cta;
+        ev[kEvKind] = (partial ? 1 : 0) | (npeer > 0 ? 2 : 0) | (static_cast<long long>(npeer) << 8);
+        ev[kEvDone] = ptx::globaltimer();
       }
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;

@@ -123,6 +123,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
   uint32_t stage = 0, phase = 0;
   for_each_segment(s, cta, P.num_ctas, P.raster_rows,
                    [&](int64_t u, int64_t tile, int64_t lb, int64_t le) {
+    long long* ev = tid == 0 ? event_slot(P, u, tile) : nullptr;
+    if (ev) ev[kEvMacStart] = ptx::globaltimer();
     double acc[2][4][4];
 #pragma unroll
     for (int i = 0; i < 2; ++i)
@@ -165,6 +167,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
     int64_t owner = u, last = u;
     if (!partial && le < s.ipt) s.peers(tile, &owner, &last);
     const int npeer = static_cast<int>(last - u);
+    if (ev) {
+      ev[kEvMacEnd] = ptx::globaltimer();
+      ev[kEvUnit] = u;
+      ev[kEvTile] = tile;
+      ev[kEvCore] = cta;
+      ev[kEvKind] = (partial ? 1 : 0) | (npeer > 0 ? 2 : 0) | (static_cast<long long>(npeer) << 8);
+    }
     if (partial) {
       double* slab = partials + s.slab_of(u) * static_cast<int64_t>(SLAB_ELEMS);
 #pragma unroll
@@ -179,12 +188,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
         signal_flag(P, P.flags + s.slab_of(u));
         if (P.trace) atomicAdd(P.trace + 4 * s.total_tiles + u, 1);
       }
+      if (ev) ev[kEvWaitEnd] = ev[kEvDone] = ptx::globaltimer();
       return;
     }
     if (npeer > 0) {
       if (tid == 0)
         for (int p = 1; p <= npeer; ++p) wait_flag(P, P.flags + s.slab_of(u + p));
       ptx::named_bar_sync(1, 128);
+      if (ev) ev[kEvWaitEnd] = ptx::globaltimer();
       // Owner fold: own accumulator, then peers in ascending id (executor.hpp:165-172).
       for (int p = 1; p <= npeer; ++p) {
         const double* slab = partials + s.slab_of(u + p) * static_cast<int64_t>(SLAB_ELEMS);
@@ -224,6 +235,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
             __stcs(dst, acc[i][j][2 * h]);
           }
         }
+    if (ev) {
+      if (npeer == 0) ev[kEvWaitEnd] = ev[kEvMacEnd];
+      ev[kEvDone] = ptx::globaltimer();
+    }
   });
 #endif
 }

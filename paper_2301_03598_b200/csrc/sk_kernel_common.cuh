@@ -40,6 +40,8 @@ struct KernelParams {
   int* err;
   int* trace;
   long long* cta_clocks;  // optional: per CTA {clock64, globaltimer} at start and end
+  long long* events;      // optional timeline: 8 int64 per (unit, segment), see event_slot
+  int64_t seg_stride;     // max tile segments of one unit (timeline indexing)
   int64_t watchdog_ns;
   int64_t raster_rows;  // data-parallel tile-row group height (1 = row-major)
 };
@@ -119,6 +121,18 @@ __device__ __forceinline__ void stamp_clock(const KernelParams& P, int slot) {
     c[0] = static_cast<long long>(clock64());
     c[1] = static_cast<long long>(ptx::globaltimer());
   }
+}
+
+// Device timeline (sk_gemm_desc.events): one record per (unit, tile segment)
+//   {unit, tile, core, kind, t_mac_start, t_mac_end, t_wait_end, t_done}
+// with kind = 1 partial | 2 owner-with-peers | npeer << 8, times in globaltimer ns.
+// Rendered as the reference's timeline CSV / Gantt (simulate.cpp:105-168).
+enum { kEvUnit = 0, kEvTile, kEvCore, kEvKind, kEvMacStart, kEvMacEnd, kEvWaitEnd, kEvDone };
+__device__ __forceinline__ long long* event_slot(const KernelParams& P, int64_t u, int64_t tile) {
+  if (!P.events) return nullptr;
+  int64_t b, e;
+  P.s.range(u, &b, &e);
+  return P.events + 8 * (u * P.seg_stride + (tile - b / P.s.ipt));
 }
 
 // Owner-side wait for one peer flag (FixupStore::wait, executor.hpp:114-118),

@@ -422,6 +422,29 @@ sk_status sk_trace_size(const sk_gemm_desc* d, int64_t* ints) {
   return SK_OK;
 }
 
+namespace {
+int64_t max_segments_per_unit(const Schedule& s) {
+  int64_t best = 1;
+  for (int64_t u = 0; u < s.grid_size; ++u) {
+    int64_t b, e;
+    s.range(u, &b, &e);
+    if (e > b) best = std::max(best, (e - 1) / s.ipt - b / s.ipt + 1);
+  }
+  return best;
+}
+}  // namespace
+
+extern "C" sk_status sk_timeline_size(const sk_gemm_desc* d, int64_t* records, int64_t* seg_stride) {
+  Kernel k;
+  Schedule s;
+  sk_status st = check_desc(d, &k, &s);
+  if (st) return st;
+  const int64_t stride = max_segments_per_unit(s);
+  if (seg_stride) *seg_stride = stride;
+  if (records) *records = s.grid_size * stride;
+  return SK_OK;
+}
+
 sk_status sk_gemm(const sk_gemm_desc* d, void* ws, size_t ws_bytes, void* stream) {
   Kernel kern;
   Schedule s;
@@ -463,6 +486,8 @@ sk_status sk_gemm(const sk_gemm_desc* d, void* ws, size_t ws_bytes, void* stream
   P.partials = wsb + L.partials_off;
   P.trace = d->trace;
   P.cta_clocks = reinterpret_cast<long long*>(d->cta_clocks);
+  P.events = reinterpret_cast<long long*>(d->events);
+  P.seg_stride = d->events ? max_segments_per_unit(s) : 1;
   P.watchdog_ns = 4000000000LL;
   P.raster_rows = 16;
   if (const char* e = getenv("SKB200_RASTER_ROWS")) P.raster_rows = std::max(1, atoi(e));

@@ -363,3 +363,40 @@ def test_random_instances_bit_exact(sk, port, var):
                   sk.hybrid(P, blk, int(rng.integers(1, 160)), sk.HybridVariant.TwoTileSkDp)):
             got = sk.execute(a, A.astype(dt), B.astype(dt), compute=ab, variant=V)
             assert np.array_equal(got, want), (trial, m, n, k, sk.strategy_name(a.strategy), a.param)
+
+
+def test_device_timeline(sk, torch_cuda, tmp_path):
+    """Per-segment device timeline -> reference Timeline CSV / Gantt formats:
+    one record per (unit, tile segment), owners with peers carry fixup events,
+    every event is inside the launch."""
+    torch = torch_cuda
+    from paper_2301_03598_b200 import timeline as tlm
+
+    problem = sk.GemmProblem(1280, 3840, 4096)
+    V = sk.Variant.TwoSM
+    blk = sk.kernel_blocking(sk.DType.BFloat16, V)
+    a = sk.stream_k(problem, blk, 74)
+    g = sk.Gemm(a, variant=V, timeline=True)
+    A = torch.randn(problem.m, problem.k, device="cuda").to(torch.bfloat16)
+    B = torch.randn(problem.k, problem.n, device="cuda").to(torch.bfloat16)
+    C = torch.empty(problem.m, problem.n, device="cuda")
+    g.run(A, B, C)
+    g.check()
+    rec = g.timeline()
+    tbl = a.range_table()
+    ipt = a.grid.iters_per_tile
+    nseg = sum((e - 1) // ipt - b // ipt + 1 for b, e in tbl if e > b)
+    assert len(rec) == nseg
+    assert (rec[:, 4] <= rec[:, 5]).all() and (rec[:, 5] <= rec[:, 6]).all() and (rec[:, 6] <= rec[:, 7]).all()
+    owners = rec[(rec[:, 3] & 2) != 0]
+    peers = sk.fixup_peers_of(a)
+    assert len(owners) == sum(len(p) > 1 for p in peers)
+    tl = tlm.from_device(rec)
+    assert tl.p == 74 and 0 < tlm.utilization(tl) <= 1.0
+    with open(tmp_path / "t.csv", "w") as f:
+        tlm.write_timeline_csv(tl, f)
+    with open(tmp_path / "t.svg", "w") as f:
+        tlm.render_gantt(tl, f)
+    head = open(tmp_path / "t.csv").readline().strip()
+    assert head == "core_id,cta_id,kind,start,end"
+    assert open(tmp_path / "t.svg").read().startswith("<svg")
