@@ -41,14 +41,25 @@ constexpr int ROWS = 128;  // rows per CTA (= TMEM lanes)
 constexpr int BN = 256;    // tile columns (MMA N)
 constexpr int BK = 64;
 constexpr int UMMA_K = 16;
-constexpr int EPI_WARPS = 4;
-#ifndef SKB200_EPI_BUFS
-#define SKB200_EPI_BUFS 2
+// Epilogue warps: 4 (one per TMEM lane quarter) or 8 (two per quarter, each
+// draining half of the 256 accumulator columns -- twice the loads/stores in
+// flight for the fixup fold and the partial/C stores).  Measured on B200
+// (profiles/r01/epilogue_warps.txt): 8 warps speed the Stream-K fold ~15 % but
+// cost data-parallel ~1 %, because end-of-kernel fixups are L2-bandwidth-bound
+// rather than latency-bound; 4 is the default.
+#ifndef SKB200_EPI_WARPS
+#define SKB200_EPI_WARPS 4
 #endif
+#ifndef SKB200_EPI_BUFS
+#define SKB200_EPI_BUFS (SKB200_EPI_WARPS == 8 ? 1 : 2)
+#endif
+constexpr int EPI_WARPS = SKB200_EPI_WARPS;
+static_assert(EPI_WARPS == 4 || EPI_WARPS == 8, "4 or 8 epilogue warps");
+constexpr int EPI_COLS = BN / (EPI_WARPS / 4);  // accumulator columns per epilogue warp
 constexpr int EPI_BUFS = SKB200_EPI_BUFS;   // 4-KB TMA-store staging boxes per epilogue warp
 constexpr int EPI_BUF_BYTES = 32 * 32 * 4;  // 32 rows x 32 fp32 = 4 KB
 constexpr int EPI_BYTES = EPI_WARPS * EPI_BUFS * EPI_BUF_BYTES;
-constexpr int NUM_THREADS = 64 + 32 * EPI_WARPS;  // 192
+constexpr int NUM_THREADS = 64 + 32 * EPI_WARPS;  // 320 (192 with 4 epilogue warps)
 constexpr int TMEM_COLS = 512;                    // 2 x 256-col accumulators
 constexpr int SLAB_ELEMS = ROWS * BN;             // fp32 partial per CTA rank
 constexpr int B_BOX_BYTES = 64 * BK * 2;          // 64 k-rows x 64 cols
@@ -275,8 +286,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       float* my_slab = partial ? partials + fidx(u) * static_cast<int64_t>(SLAB_ELEMS) : nullptr;
       // 64 columns (two 32-column chunks) per step: one tcgen05.ld.x64, 16 float4
       // of peer slab in flight per thread, two 32x32 TMA-store boxes.
+      const int c_lo = static_cast<int>((warp - 2) / 4) * (EPI_COLS / 32);
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; c += 2) {
+      for (int c = c_lo; c < c_lo + EPI_COLS / 32; c += 2) {
         float v[64];
         ptx::tmem_ld64(tsrc + c * 32, v);
         if (partial) {
