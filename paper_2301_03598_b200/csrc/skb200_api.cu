@@ -489,7 +489,14 @@ sk_status sk_gemm(const sk_gemm_desc* d, void* ws, size_t ws_bytes, void* stream
   P.events = reinterpret_cast<long long*>(d->events);
   P.seg_stride = d->events ? max_segments_per_unit(s) : 1;
   P.watchdog_ns = 4000000000LL;
-  P.raster_rows = 16;
+  // Raster group height: the group's A panels (rows x BLK_M x k elements) are
+  // kept near 32 MB so they stay L2-resident while B streams through; measured
+  // best at 8192^3: 16 rows (1-SM), 8 rows (2-SM) (profiles/r01/raster_rows.txt).
+  {
+    const double panel = static_cast<double>(d->blocking.blk_m) * static_cast<double>(d->problem.k) *
+                         static_cast<double>(dtype_size(d->ab_type));
+    P.raster_rows = std::max<int64_t>(1, static_cast<int64_t>((32.0 * 1024 * 1024) / panel));
+  }
   if (const char* e = getenv("SKB200_RASTER_ROWS")) P.raster_rows = std::max(1, atoi(e));
   const int64_t units = std::max<int64_t>(s.grid_size, 1);
   const int64_t cap = d->num_ctas > 0 ? d->num_ctas : info.sms / P.ranks;
