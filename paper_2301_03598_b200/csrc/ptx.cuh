@@ -126,6 +126,23 @@ __device__ __forceinline__ uint64_t policy_evict_normal() {
   asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+// 0 normal, 1 evict_first, 2 evict_last
+__device__ __forceinline__ uint64_t make_policy(int kind) {
+  return kind == 1 ? policy_evict_first() : (kind == 2 ? policy_evict_last() : policy_evict_normal());
+}
+__device__ __forceinline__ void tma_store_2d_hint(const CUtensorMap* m, const void* src, int32_t c0,
+                                                  int32_t c1, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%1, %2}], [%3], %4;" ::"l"(
+          reinterpret_cast<uint64_t>(m)),
+      "r"(c0), "r"(c1), "r"(smem_u32(src)), "l"(policy)
+      : "memory");
+}
 
 // ---------------------------------------------------------------- tcgen05 / TMEM
 template <int CG>

@@ -180,7 +180,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (warp == 0) {
     // ===================== TMA producer (every CTA of the pair) =====================
     if (lane == 0) {
-      const uint64_t pol = ptx::policy_evict_last();
+      const uint64_t pol_a = ptx::make_policy(P.l2_policy[0]);
+      const uint64_t pol_b = ptx::make_policy(P.l2_policy[1]);
       uint32_t stage = 0, phase = 0;
       for_each_segment(s, cta, P.num_ctas, P.raster_rows,
                        [&](int64_t, int64_t tile, int64_t lb, int64_t le) {
@@ -193,18 +194,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           uint8_t* b_dst = sB + stage * K::B_STAGE;
           if constexpr (CG == 1) {
             ptx::mbar_expect_tx(&full_bar[stage], K::STAGE);
-            ptx::tma_load_2d(a_dst, &tmA, &full_bar[stage], k0, m0, pol);
+            ptx::tma_load_2d(a_dst, &tmA, &full_bar[stage], k0, m0, pol_a);
 #pragma unroll
             for (int i = 0; i < K::B_COLS / 64; ++i)
-              ptx::tma_load_2d(b_dst + i * B_BOX_BYTES, &tmB, &full_bar[stage], n0 + 64 * i, k0, pol);
+              ptx::tma_load_2d(b_dst + i * B_BOX_BYTES, &tmB, &full_bar[stage], n0 + 64 * i, k0, pol_b);
           } else {
             // Both CTAs' bytes land on the leader's full barrier; only the leader arrives.
             if (leader_cta) ptx::mbar_expect_tx(&full_bar[stage], 2 * K::STAGE);
             const uint32_t fb = mapa(&full_bar[stage], 0);
-            tma_load_2d_to_leader(a_dst, &tmA, fb, k0, m0, pol);
+            tma_load_2d_to_leader(a_dst, &tmA, fb, k0, m0, pol_a);
 #pragma unroll
             for (int i = 0; i < K::B_COLS / 64; ++i)
-              tma_load_2d_to_leader(b_dst + i * B_BOX_BYTES, &tmB, fb, n0 + 64 * i, k0, pol);
+              tma_load_2d_to_leader(b_dst + i * B_BOX_BYTES, &tmB, fb, n0 + 64 * i, k0, pol_b);
           }
           if (++stage == K::STAGES) {
             stage = 0;
@@ -261,6 +262,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const bool leader = (threadIdx.x == 64);
     float* stage_buf = sEpi + (warp - 2) * EPI_BUFS * (EPI_BUF_BYTES / 4);
     float* partials = static_cast<float*>(P.partials);
+    const uint64_t pol_c = ptx::make_policy(P.l2_policy[2]);
     uint32_t acc = 0, acc_phase = 0, nstores = 0;
     // flag / slab index of a (unit, rank): each CTA of a pair runs its own protocol
     auto fidx = [&](int64_t u) { return s.slab_of(u) * CG + rank; };
@@ -339,7 +341,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             ptx::fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
-              ptx::tma_store_2d(&tmC, buf, n0 + (c + h) * 32, m0 + static_cast<int32_t>(q * 32));
+              ptx::tma_store_2d_hint(&tmC, buf, n0 + (c + h) * 32, m0 + static_cast<int32_t>(q * 32),
+                                     pol_c);
               ptx::tma_store_commit();
             }
             ++nstores;
