@@ -181,12 +181,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // ===================== TMA producer (every CTA of the pair) =====================
     if (lane == 0) {
       const uint64_t pol_a = ptx::make_policy(P.l2_policy[0]);
-      const uint64_t pol_b = ptx::make_policy(P.l2_policy[1]);
+      const uint64_t pol_b_dp = ptx::make_policy(P.l2_policy[1]);
+      const uint64_t pol_b_sk = ptx::make_policy(P.l2_policy[3]);
       uint32_t stage = 0, phase = 0;
       for_each_segment(s, cta, P.num_ctas, P.raster_rows,
-                       [&](int64_t, int64_t tile, int64_t lb, int64_t le) {
+                       [&](int64_t u, int64_t tile, int64_t lb, int64_t le) {
         const int32_t m0 = static_cast<int32_t>((tile / s.tiles_n) * (ROWS * CG) + rank * ROWS);
         const int32_t n0 = static_cast<int32_t>((tile % s.tiles_n) * BN + rank * K::B_COLS);
+        // B panels stream through a data-parallel wave but are revisited at
+        // unrelated k offsets by Stream-K units: separate L2 priorities.
+        const bool sk_unit = s.strategy == kFixedSplit || s.bal.contains_id(u);
+        const uint64_t pol_b = sk_unit ? pol_b_sk : pol_b_dp;
         for (int64_t kb = lb; kb < le; ++kb) {
           ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
           const int32_t k0 = static_cast<int32_t>(kb * BK);

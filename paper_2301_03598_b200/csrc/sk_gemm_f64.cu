@@ -85,11 +85,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
   __syncthreads();
   ptx::grid_dependency_wait();
   ptx::launch_dependents();
+  stamp_clock(P, 0);
 
   if (warp == CONSUMERS) {
     // ===================== TMA producer =====================
     if (lane == 0) {
-      const uint64_t pol = ptx::policy_evict_last();
+      const uint64_t pol_a = ptx::make_policy(P.l2_policy[0]);
+      const uint64_t pol_b = ptx::make_policy(P.l2_policy[1]);
       uint32_t stage = 0, phase = 0;
       for_each_segment(s, cta, P.num_ctas, P.raster_rows,
                        [&](int64_t, int64_t tile, int64_t lb, int64_t le) {
@@ -100,11 +102,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
           ptx::mbar_expect_tx(&full_bar[stage], STAGE_BYTES);
           uint8_t* st = smem + stage * STAGE_BYTES;
           const int32_t k0 = static_cast<int32_t>(kb * BK);
-          ptx::tma_load_2d(st, &tmA, &full_bar[stage], k0, m0, pol);
+          ptx::tma_load_2d(st, &tmA, &full_bar[stage], k0, m0, pol_a);
 #pragma unroll
           for (int j = 0; j < 4; ++j)
             ptx::tma_load_2d(st + A_BYTES + j * B_BOX_BYTES, &tmB, &full_bar[stage], n0 + 16 * j, k0,
-                             pol);
+                             pol_b);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -240,6 +242,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
       ev[kEvDone] = ptx::globaltimer();
     }
   });
+  stamp_clock(P, 1);
 #endif
 }
 

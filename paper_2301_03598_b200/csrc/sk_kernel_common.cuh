@@ -44,7 +44,8 @@ struct KernelParams {
   int64_t seg_stride;     // max tile segments of one unit (timeline indexing)
   int64_t watchdog_ns;
   int64_t raster_rows;  // data-parallel tile-row group height (1 = row-major)
-  int32_t l2_policy[3];  // L2 eviction priority for A loads, B loads, C stores:
+  int32_t l2_policy[4];  // L2 eviction priority for A loads, B loads (data-parallel
+                         // units), C stores, B loads (Stream-K / fixed-split units):
                          // 0 normal, 1 evict_first, 2 evict_last
 };
 

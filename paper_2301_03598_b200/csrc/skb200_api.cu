@@ -506,8 +506,9 @@ sk_status sk_gemm(const sk_gemm_desc* d, void* ws, size_t ws_bytes, void* stream
   P.l2_policy[0] = 2;
   P.l2_policy[1] = 1;
   P.l2_policy[2] = 1;
+  P.l2_policy[3] = 2;
   if (const char* e = getenv("SKB200_L2_POLICY"))
-    sscanf(e, "%d,%d,%d", &P.l2_policy[0], &P.l2_policy[1], &P.l2_policy[2]);
+    sscanf(e, "%d,%d,%d,%d", &P.l2_policy[0], &P.l2_policy[1], &P.l2_policy[2], &P.l2_policy[3]);
   const int64_t units = std::max<int64_t>(s.grid_size, 1);
   const int64_t cap = d->num_ctas > 0 ? d->num_ctas : info.sms / P.ranks;
   P.num_ctas = std::min<int64_t>(units, std::min<int64_t>(cap, info.sms / P.ranks));
