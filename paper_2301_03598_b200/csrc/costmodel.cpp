@@ -211,17 +211,23 @@ sk_status sk_select_schedule(const sk_cost_params* c, const sk_tile_grid_t* g, i
   if (!c || !valid_grid(g) || p < 1 || !strategy || !param) return SK_EINVAL;
   double t_dp;
   sk_predict_schedule(c, g, SK_DATA_PARALLEL, 1, p, &t_dp);
-  int64_t gbest;
-  sk_cost_params nomargin = *c;
-  nomargin.margin = 0.0;
-  sk_select_grid_size(&nomargin, g, p, &gbest);
-  int32_t best_s = SK_STREAM_K;
-  int64_t best_p = gbest;
-  double bt;
-  sk_predict_time(c, g, gbest, p, &bt);
-  if (gbest == std::min(g->total_tiles, g->total_iters)) {
-    best_s = SK_DATA_PARALLEL;
-    best_p = 1;
+  int32_t best_s = SK_DATA_PARALLEL;
+  int64_t best_p = 1;
+  double bt = t_dp;
+  // Basic Stream-K only while its units stay within ~one tile wave (t < 2p):
+  // beyond that every unit spans several tiles at unrelated k offsets, which
+  // defeats L2 reuse (not in the model), and the paper's two-tile hybrid takes
+  // over; measured: profiles/r01/sweep_corpus_seed0_1000_2sm.csv.
+  if (g->total_tiles < 2 * p) {
+    int64_t gbest;
+    sk_cost_params nomargin = *c;
+    nomargin.margin = 0.0;
+    sk_select_grid_size(&nomargin, g, p, &gbest);
+    if (gbest != std::min(g->total_tiles, g->total_iters)) {
+      best_s = SK_STREAM_K;
+      best_p = gbest;
+      sk_predict_time(c, g, gbest, p, &bt);
+    }
   }
   if (g->total_tiles > p && g->total_tiles % p != 0) {
     double t2;
