@@ -32,7 +32,7 @@ import paper_2301_03598_b200 as sk
 
 SCHEMA = "# schema=sk_b200/1"
 COLUMNS = ["m", "n", "k", "tiles_m", "tiles_n", "t", "iters_per_tile", "strategy", "param", "g",
-           "variant", "dtype",
+           "schedule", "variant", "dtype",
            "copies", "l2_cold", "time_us", "tflops"]
 L2_BYTES = 126 * 1024 * 1024
 
@@ -116,7 +116,10 @@ class ShapeTimer:
                     gemm.run(self.A[i], self.B[i], self.C)
         torch.cuda.synchronize()
         best = float("inf")
-        for _ in range(reps):
+        r = 0
+        # best of `reps` replays; short launches (< 50 us) get 3x more replays
+        # because their run-to-run noise is ~10 %
+        while r < reps or (best < 50.0 and r < 3 * reps):
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record()
@@ -124,6 +127,7 @@ class ShapeTimer:
             e1.record()
             torch.cuda.synchronize()
             best = min(best, e0.elapsed_time(e1) * 1e3 / self.copies)
+            r += 1
         gemm.check()
         return best
 
@@ -150,6 +154,7 @@ def run(shapes, names, variant, dtype, rank=0, world=1, log_every=0, params=None
             rows.append({"idx": idx, "m": m, "n": n, "k": k, "t": a.grid.total_tiles,
                          "iters_per_tile": a.grid.iters_per_tile,
                          "strategy": getattr(a, "label", sk.strategy_name(a.strategy)),
+                         "schedule": sk.strategy_name(a.strategy),
                          "param": a.param, "tiles_m": a.grid.tiles_m, "tiles_n": a.grid.tiles_n,
                          "g": a.grid_size,
                          "variant": "dmma" if dtype == "fp64" else (
