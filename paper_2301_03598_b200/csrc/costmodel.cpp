@@ -290,7 +290,7 @@ sk_status sk_default_cost_params(sk_dtype ab_type, sk_variant variant, sk_cost_p
   } else if (variant == SK_VARIANT_2SM || variant == SK_VARIANT_AUTO) {
     c = {3.9049, 0.9955, 0.4063, 0.3098, 2.3291, 3.3913, 0.2, 0.0};
   } else {
-    c = {3.9049, 0.9955, 0.4063, 0.1549, 2.3291, 3.3913, 0.2, 0.0};
+    c = {4.2166, 0.24668, 1.8380, 0.42998, 2.6520, 2.8518, 0.2, 0.0};  // costmodel_1sm.json
   }
   *out = c;
   return SK_OK;
