@@ -202,10 +202,14 @@ sk_status sk_gemm(const sk_gemm_desc* desc, void* workspace, size_t workspace_by
 
 /* ---- reference-facing drop-in of streamk::execute<T> ------------------- */
 /* Host buffers in, host C out (tight row-major, ld = cols), synchronous.
- * host_type: SK_BFLOAT16 / SK_FLOAT16 (raw 16-bit), SK_FLOAT32 (values rounded
- * to compute_type on the device), SK_FLOAT64 (compute_type must be FLOAT64).
- * C is float32 for 16-bit compute, float64 for FP64.  Device buffers, workspace
- * and the stream are cached per host thread.  device < 0 = current device. */
+ * compute_type BFLOAT16/FLOAT16: host_type is the same 16-bit type (raw bits)
+ *   or FLOAT32 (rounded to nearest on the device); C is float32.
+ * compute_type FLOAT64 (tensor-core DMMA): host_type FLOAT64 (C double),
+ *   FLOAT32 (widened exactly, C float -- execute<float> without input rounding)
+ *   or INT64 (C int64, exact; SK_EUNSUPPORTED unless max|A| max|B| k < 2^53 --
+ *   execute<int64_t>).
+ * Device buffers, workspace and the stream are cached per host thread.
+ * device < 0 = current device. */
 sk_status sk_execute(const sk_problem* problem, const sk_blocking* blocking,
                      sk_strategy strategy, int64_t param, sk_dtype host_type,
                      sk_dtype compute_type, int32_t variant, const void* A, const void* B,

@@ -539,15 +539,21 @@ def _host_type(arr: np.ndarray) -> DType:
         return DType.Float16
     if arr.dtype == np.uint16:  # raw bfloat16 bits
         return DType.BFloat16
+    if arr.dtype == np.int64:
+        return DType.Int64
     raise ValueError(f"unsupported host dtype {arr.dtype}")
 
 
 def execute(a: WorkAssignment, A: np.ndarray, B: np.ndarray, compute: DType = DType.BFloat16,
             variant: Variant = Variant.Auto, device: int = -1) -> np.ndarray:
     """Drop-in of streamk::execute<T> (executor.hpp:130-207): host A (m x k),
-    B (k x n) in, new host C (m x n) out, synchronous.  A/B may be float32
-    (rounded to `compute` on the device), float16, uint16 (bfloat16 bits) or
-    float64 (compute must be Float64).  C is float32 (float64 for FP64)."""
+    B (k x n) in, new host C (m x n) out, synchronous.
+    compute BFloat16/Float16: A/B float32 (rounded on the device), float16 or
+    uint16 (bfloat16 bits); C float32.
+    compute Float64 (DMMA): A/B float64, float32 (execute<float>, widened
+    exactly, C float32) or int64 (execute<int64_t>, exact, C int64; refused
+    unless max|A| max|B| k < 2^53).  The blocking must be the kernel tile of
+    `compute` (kernel_blocking)."""
     p = a.problem
     if A.shape != (p.m, p.k) or B.shape != (p.k, p.n):
         raise ValueError("execute: matrix shapes do not match assignment")
@@ -558,7 +564,11 @@ def execute(a: WorkAssignment, A: np.ndarray, B: np.ndarray, compute: DType = DT
         raise ValueError("execute: A and B host dtypes differ")
     A = np.ascontiguousarray(A)
     B = np.ascontiguousarray(B)
-    Cm = np.empty((p.m, p.n), np.float64 if compute == DType.Float64 else np.float32)
+    if compute == DType.Float64:  # C in the caller's type: execute<double|float|int64_t>
+        cdt = {DType.Float64: np.float64, DType.Float32: np.float32, DType.Int64: np.int64}[ht]
+    else:
+        cdt = np.float32
+    Cm = np.empty((p.m, p.n), cdt)
     _check(lib().sk_execute(C.byref(p._c()), C.byref(a.blocking._c()), int(a.strategy), a.param,
                             int(ht), int(compute), int(variant), A.ctypes.data_as(C.c_void_p),
                             B.ctypes.data_as(C.c_void_p), Cm.ctypes.data_as(C.c_void_p), device),

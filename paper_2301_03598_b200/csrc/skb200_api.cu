@@ -37,6 +37,8 @@ cudaError_t f64_max_ctas_per_sm(int* out);
 cudaError_t launch_f64(const CUtensorMap& a, const CUtensorMap& b, double* C, int64_t ldc,
                        const KernelParams& p, int grid, cudaStream_t stream);
 // sk_convert.cu
+cudaError_t launch_convert(int kind, const void* src, int64_t ld_src, void* dst, int64_t ld_dst,
+                           int64_t rows, int64_t cols, cudaStream_t stream);
 cudaError_t launch_f32_to_16(const float* src, void* dst, int64_t rows, int64_t cols,
                              int64_t ld_dst, bool bf16, cudaStream_t stream);
 }  // namespace skb200
@@ -616,7 +618,22 @@ extern "C" sk_status sk_execute(const sk_problem* p, const sk_blocking* b, sk_st
   const bool is16 = compute_type != SK_FLOAT64;
   if (is16 && !(host_type == compute_type || host_type == SK_FLOAT32))
     return fail(SK_EINVAL, "host_type must equal compute_type or be FLOAT32");
-  if (!is16 && host_type != SK_FLOAT64) return fail(SK_EINVAL, "FP64 compute needs FP64 host data");
+  if (!is16 && host_type != SK_FLOAT64 && host_type != SK_FLOAT32 && host_type != SK_INT64)
+    return fail(SK_EINVAL, "FP64 compute takes FLOAT64, FLOAT32 or INT64 host data");
+  if (!is16 && host_type == SK_INT64) {
+    // execute<int64_t> on the FP64 tensor path is exact while every partial sum
+    // stays below 2^53: max|A| * max|B| * k < 2^53 (the reference band is [-64, 63]).
+    auto maxabs = [](const void* p, int64_t cnt) {
+      const int64_t* v = static_cast<const int64_t*>(p);
+      long double mx = 0;
+      for (int64_t i = 0; i < cnt; ++i) mx = std::max(mx, std::fabs(static_cast<long double>(v[i])));
+      return mx;
+    };
+    const long double bound = maxabs(A, p->m * p->k) * maxabs(B, p->k * p->n) *
+                              static_cast<long double>(p->k);
+    if (bound >= 9007199254740992.0L)
+      return fail(SK_EUNSUPPORTED, "int64 operands exceed the exact fp64 range (max|A|max|B|k >= 2^53)");
+  }
 
   int dev = device;
   if (dev < 0) SK_CUDA(cudaGetDevice(&dev));
@@ -671,6 +688,16 @@ extern "C" sk_status sk_execute(const sk_problem* p, const sk_blocking* b, sk_st
     SK_CUDA(launch_f32_to_16(stg, X.buf[0], m, k, lda, compute_type == SK_BFLOAT16, s));
     SK_CUDA(cudaMemcpyAsync(stg, B, sizeof(float) * k * n, cudaMemcpyHostToDevice, s));
     SK_CUDA(launch_f32_to_16(stg, X.buf[1], k, n, ldb, compute_type == SK_BFLOAT16, s));
+  } else if (!is16 && host_type != SK_FLOAT64) {
+    // execute<float> / execute<int64_t> on the FP64 path: widen exactly on the device.
+    const size_t hs = dtype_size(host_type);
+    st = X.ensure(4, static_cast<size_t>(std::max(std::max(m * k, k * n), m * n)) * 8);
+    if (st) return st;
+    const int kind = host_type == SK_FLOAT32 ? 0 : 1;
+    SK_CUDA(cudaMemcpyAsync(X.buf[4], A, hs * m * k, cudaMemcpyHostToDevice, s));
+    SK_CUDA(launch_convert(kind, X.buf[4], k, X.buf[0], lda, m, k, s));
+    SK_CUDA(cudaMemcpyAsync(X.buf[4], B, hs * k * n, cudaMemcpyHostToDevice, s));
+    SK_CUDA(launch_convert(kind, X.buf[4], n, X.buf[1], ldb, k, n, s));
   } else {
     SK_CUDA(cudaMemcpy2DAsync(X.buf[0], lda * esz, A, k * esz, k * esz, m, cudaMemcpyHostToDevice, s));
     SK_CUDA(cudaMemcpy2DAsync(X.buf[1], ldb * esz, B, n * esz, n * esz, k, cudaMemcpyHostToDevice, s));
@@ -680,7 +707,14 @@ extern "C" sk_status sk_execute(const sk_problem* p, const sk_blocking* b, sk_st
   d.C = X.buf[2];
   st = sk_gemm(&d, X.buf[3], ws_bytes, s);
   if (st) return st;
-  SK_CUDA(cudaMemcpy2DAsync(C, n * csz, X.buf[2], ldc * csz, n * csz, m, cudaMemcpyDeviceToHost, s));
+  if (!is16 && host_type != SK_FLOAT64) {
+    // narrow the fp64 C to the caller's element type, tightly packed, then D2H
+    const size_t hs = dtype_size(host_type);
+    SK_CUDA(launch_convert(host_type == SK_FLOAT32 ? 2 : 3, X.buf[2], ldc, X.buf[4], n, m, n, s));
+    SK_CUDA(cudaMemcpyAsync(C, X.buf[4], hs * m * n, cudaMemcpyDeviceToHost, s));
+  } else {
+    SK_CUDA(cudaMemcpy2DAsync(C, n * csz, X.buf[2], ldc * csz, n * csz, m, cudaMemcpyDeviceToHost, s));
+  }
   return sk_workspace_check(X.buf[3], s);
 }
 

@@ -400,3 +400,33 @@ def test_device_timeline(sk, torch_cuda, tmp_path):
     head = open(tmp_path / "t.csv").readline().strip()
     assert head == "core_id,cta_id,kind,start,end"
     assert open(tmp_path / "t.svg").read().startswith("<svg")
+
+
+def test_execute_drop_in_all_reference_types(sk, port, ref):
+    """execute<int64_t>, execute<float>, execute<double> of the reference, via the
+    FP64 tensor path: int64 bit-exact, float/double within the reference's bound,
+    each against the reference's own executor on the same inputs."""
+    import oracle
+
+    blk = sk.kernel_blocking(sk.DType.Float64)
+    m, n, k = 384, 320, 512
+    for strat, param in (("stream_k", 37), ("two_tile_sk_dp", 11), ("fixed_split", 3), ("data_parallel", 1)):
+        a = sk._assignment(sk.Strategy(NAMES.index(strat)), sk.GemmProblem(m, n, k), blk, param)
+        Ai, Bi = int_operands(port, m, n, k, 5)
+        Ci = sk.execute(a, Ai, Bi, compute=sk.DType.Float64)
+        assert Ci.dtype == np.int64
+        assert np.array_equal(Ci, ref.execute(strat, param, Ai, Bi, 64, 64, 16, threads=8))
+        Af = port.random_matrix(m, k, 7, "float32")
+        Bf = port.random_matrix(k, n, 8, "float32")
+        Cf = sk.execute(a, Af, Bf, compute=sk.DType.Float64)
+        assert Cf.dtype == np.float32
+        ok, _, mr = oracle.verify(Cf, ref.execute(strat, param, Af, Bf, 64, 64, 16, threads=8), k, EPS32)
+        assert ok, mr
+        Ad = port.random_matrix(m, k, 9, "float64")
+        Bd = port.random_matrix(k, n, 10, "float64")
+        Cd = sk.execute(a, Ad, Bd, compute=sk.DType.Float64)
+        ok, _, mr = oracle.verify(Cd, ref.execute(strat, param, Ad, Bd, 64, 64, 16, threads=8), k, EPS64)
+        assert ok, mr
+    big = np.full((8, 8), 2 ** 40, np.int64)
+    with pytest.raises(sk.UnsupportedError):
+        sk.execute(sk.data_parallel(sk.GemmProblem(8, 8, 8), blk), big, big, compute=sk.DType.Float64)
