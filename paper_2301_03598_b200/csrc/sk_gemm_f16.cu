@@ -217,7 +217,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             phase ^= 1;
           }
         }
-      });
+      }, P.sk_first != 0);
     }
     __syncwarp();
   } else if (warp == 1) {
@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         else ptx::umma_commit_mc(&tfull_bar[acc], 0x3);
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
-      });
+      }, P.sk_first != 0);
     }
     __syncwarp();
   } else {
@@ -391,7 +391,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
-    });
+    }, P.sk_first != 0);
     if (lane == 0) ptx::tma_store_wait_all<0>();
     __syncwarp();
   }

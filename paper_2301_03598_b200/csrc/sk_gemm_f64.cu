@@ -112,7 +112,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
             phase ^= 1;
           }
         }
-      });
+      }, P.sk_first != 0);
     }
     return;
   }
@@ -241,7 +241,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
       if (npeer == 0) ev[kEvWaitEnd] = ev[kEvMacEnd];
       ev[kEvDone] = ptx::globaltimer();
     }
-  });
+  }, P.sk_first != 0);
   stamp_clock(P, 1);
 #endif
 }

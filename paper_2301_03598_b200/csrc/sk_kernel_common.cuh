@@ -44,6 +44,7 @@ struct KernelParams {
   int64_t seg_stride;     // max tile segments of one unit (timeline indexing)
   int64_t watchdog_ns;
   int64_t raster_rows;  // data-parallel tile-row group height (1 = row-major)
+  int32_t sk_first;      // TwoTileSkDp: run the SK region before the DP waves
   int32_t l2_policy[4];  // L2 eviction priority for A loads, B loads (data-parallel
                          // units), C stores, B loads (Stream-K / fixed-split units):
                          // 0 normal, 1 evict_first, 2 evict_last
@@ -96,7 +97,7 @@ __device__ __forceinline__ void run_unit(const Schedule& s, int64_t u, F& f) {
 
 template <class F>
 __device__ __forceinline__ void for_each_segment(const Schedule& s, int64_t cta, int64_t P,
-                                                 int64_t raster_rows, F&& f) {
+                                                 int64_t raster_rows, F&& f, bool sk_first = false) {
   auto dp_phase = [&] {
     for (int64_t i = cta; i < s.dp_tiles; i += P) run_unit(s, s.dp_id0 + raster_tile(s, i, raster_rows), f);
   };
@@ -107,10 +108,10 @@ __device__ __forceinline__ void for_each_segment(const Schedule& s, int64_t cta,
     desc_phase(0, s.grid_size);
   } else if (s.bal.count == 0) {
     dp_phase();
-  } else if (s.dp_id0 > s.bal.first_id) {  // TwoTileSkDp: DP ids above the SK ids
+  } else if (s.dp_id0 > s.bal.first_id && !sk_first) {  // TwoTileSkDp, DP wave(s) first
     dp_phase();
     desc_phase(s.bal.first_id, s.bal.first_id + s.bal.count);
-  } else {  // StreamK, DpOneTileSk: SK ids above the DP ids
+  } else {  // StreamK, DpOneTileSk, TwoTileSkDp with the SK region first (Fig. 4c)
     desc_phase(s.bal.first_id, s.bal.first_id + s.bal.count);
     dp_phase();
   }
