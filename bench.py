@@ -220,12 +220,23 @@ def main():
 
     import paper_2301_03598_b200 as sk
 
+    ndev = torch.cuda.device_count()
+    # One rank per GPU.  More ranks than GPUs only happens when the multi-rank
+    # path is exercised on a 1-GPU box: ranks then share devices and the two
+    # timing collectives (barrier, max-reduction) use gloo, since NCCL refuses
+    # two ranks on one GPU.  The GEMM data path has no collective either way.
+    local = local % max(ndev, 1)
     torch.cuda.set_device(local)
     dist = None
+    coll_dev = "cuda"
     if world > 1:
         import torch.distributed as dist_
 
-        dist_.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if world <= ndev:
+            dist_.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist_.init_process_group("gloo")
+            coll_dev = "cpu"
         dist = dist_
 
     ab = {"bf16": sk.DType.BFloat16, "fp16": sk.DType.Float16, "fp64": sk.DType.Float64}[args.dtype]
@@ -268,7 +279,7 @@ def main():
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / steps
         if dist:
-            t = torch.tensor([ms], device="cuda")
+            t = torch.tensor([ms], device=coll_dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
         return ms
@@ -330,7 +341,7 @@ def main():
             e2e_step()  # synchronous: H2D + kernel + D2H + status read
         dt = (time.perf_counter() - t0) / steps_e2e
         if dist:
-            t = torch.tensor([dt], device="cuda")
+            t = torch.tensor([dt], device=coll_dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             dt = float(t.item())
         e2e = {"value": flops * world / dt / 1e12, "unit": "TFLOP/s",
