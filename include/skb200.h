@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define SKB200_ABI_VERSION 1
+#define SKB200_ABI_VERSION 2
 
 typedef enum sk_status {
   SK_OK = 0,
@@ -57,7 +57,10 @@ typedef enum sk_strategy {
   SK_FIXED_SPLIT = 1,   /* param = s */
   SK_STREAM_K = 2,      /* param = g */
   SK_DP_ONE_TILE_SK = 3, /* param = p */
-  SK_TWO_TILE_SK_DP = 4  /* param = p */
+  SK_TWO_TILE_SK_DP = 4, /* param = p */
+  SK_EXPLICIT = 5        /* an arbitrary range table (sk_gemm_desc.ranges / sk_execute_ranges):
+                            a WorkAssignment no closed form produces, e.g. from from_text
+                            (types.cpp:109-123).  Not accepted by sk_schedule/sk_fixup_peers. */
 } sk_strategy;
 
 typedef enum sk_dtype {
@@ -112,7 +115,24 @@ typedef struct sk_gemm_desc {
                            {clock64 start, globaltimer ns start, clock64 end, globaltimer end} */
   int64_t* events;      /* optional device timeline, 8 int64 per record, see sk_timeline_size:
                            {unit, tile, core, kind, t_mac_start, t_mac_end, t_wait_end, t_done},
-                           kind = 1 partial | 2 owner with peers | npeer << 8; ns */
+                           kind = 1 partial | 2 owner with peers | npeer << 8 |
+                           smid << 16 (SM that ran the epilogue); ns */
+  /* ABI v2: strategy == SK_EXPLICIT only.  HOST table [num_ranges][2] of
+   * (iter_begin, iter_end), row index == cta_id, executed like execute<T> executes
+   * assignment.ranges (executor.hpp:147-185).  Validated on every call:
+   *   0 <= iter_begin <= iter_end <= total_iters, else SK_EINVAL (mac_loop's
+   *   invalid_argument, executor.hpp:63-68);
+   *   a tile started (local k = 0) by two ranges -> SK_EINVAL (the reference
+   *   would wait forever: each starter waits on the other);
+   *   a starter with a lower-id peer -> SK_EUNSUPPORTED (its wait would point
+   *   to a lower id, which a persistent grid cannot order; every closed-form
+   *   schedule has all waits pointing up, executor.hpp:124-129).
+   * Tiles no range starts are not written (the reference leaves them zero in its
+   * fresh C; sk_execute_ranges zero-fills).  The table (ranges + peer lists) is
+   * copied into the workspace tail (sk_workspace_size counts it) and re-copied
+   * only when the workspace last ran a different table. */
+  const int64_t* ranges;
+  int64_t num_ranges;
 } sk_gemm_desc;
 
 const char* sk_status_string(sk_status status);
@@ -214,6 +234,18 @@ sk_status sk_execute(const sk_problem* problem, const sk_blocking* blocking,
                      sk_strategy strategy, int64_t param, sk_dtype host_type,
                      sk_dtype compute_type, int32_t variant, const void* A, const void* B,
                      void* C, int32_t device);
+/* sk_execute over an explicit range table ([num_ranges][2], see sk_gemm_desc.ranges):
+ * the drop-in for execute<T> on an arbitrary WorkAssignment.  C is zero-filled
+ * first when some tile has no starting range, like the reference's fresh C. */
+sk_status sk_execute_ranges(const sk_problem* problem, const sk_blocking* blocking,
+                            const int64_t* ranges, int64_t num_ranges, sk_dtype host_type,
+                            sk_dtype compute_type, int32_t variant, const void* A,
+                            const void* B, void* C, int32_t device);
+/* fixup_peers_of (decompose.cpp:123-136) of an explicit range table, CSR as in
+ * sk_fixup_peers; validates the ranges like sk_gemm (bounds only). */
+sk_status sk_fixup_peers_ranges(const sk_problem* problem, const sk_blocking* blocking,
+                                const int64_t* ranges, int64_t num_ranges, int64_t* offsets,
+                                int64_t* ids, int64_t capacity, int64_t* nnz);
 /* Releases the calling thread's sk_execute cache. */
 void sk_execute_release(void);
 

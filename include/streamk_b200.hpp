@@ -51,7 +51,7 @@ inline sk_strategy to_sk(streamk::Strategy s) {
 }
 
 // The closed-form knob (s, g or p) whose schedule reproduces a.ranges exactly;
-// throws invalid_argument for a range table no decomposition produces.
+// 0 for a range table no decomposition produces (run as SK_EXPLICIT).
 inline int64_t knob(const streamk::WorkAssignment& a) {
   const sk_problem pr = to_sk(a.problem);
   const sk_blocking bl = to_sk(a.blocking);
@@ -79,7 +79,7 @@ inline int64_t knob(const streamk::WorkAssignment& a) {
       for (int64_t p = 1; p <= a.grid_size; ++p)
         if (matches(p)) return p;
   }
-  throw std::invalid_argument("execute: assignment is not a closed-form schedule");
+  return 0;
 }
 
 template <typename T>
@@ -102,8 +102,23 @@ streamk::Matrix<T> execute(const streamk::WorkAssignment& a, const streamk::Matr
   const sk_problem pr = to_sk(a.problem);
   const sk_blocking bl = to_sk(a.blocking);
   streamk::Matrix<T> C(a.problem.m, a.problem.n);
-  throw_on(sk_execute(&pr, &bl, to_sk(a.strategy), knob(a), host, compute, SK_VARIANT_AUTO,
-                      A.data.data(), B.data.data(), C.data.data(), device));
+  if (const int64_t prm = knob(a)) {
+    throw_on(sk_execute(&pr, &bl, to_sk(a.strategy), prm, host, compute, SK_VARIANT_AUTO,
+                        A.data.data(), B.data.data(), C.data.data(), device));
+    return C;
+  }
+  // Any other table (e.g. from from_text): ranges by position, as execute<T> reads
+  // them (executor.hpp:148); fixup_peers_of keys by cta_id, so they must agree.
+  std::vector<int64_t> tbl(2 * a.ranges.size());
+  for (size_t i = 0; i < a.ranges.size(); ++i) {
+    if (a.ranges[i].cta_id != static_cast<streamk::index_t>(i))
+      throw std::invalid_argument("execute: range table cta_ids must be 0..g-1 in order");
+    tbl[2 * i] = a.ranges[i].iter_begin;
+    tbl[2 * i + 1] = a.ranges[i].iter_end;
+  }
+  throw_on(sk_execute_ranges(&pr, &bl, tbl.data(), static_cast<int64_t>(a.ranges.size()), host,
+                             compute, SK_VARIANT_AUTO, A.data.data(), B.data.data(),
+                             C.data.data(), device));
   return C;
 }
 

@@ -194,6 +194,30 @@ class Oracle:
             raise OracleError(st, "execute")
         return Cm
 
+    def execute_ranges(self, ranges: np.ndarray, A: np.ndarray, B: np.ndarray, bm, bn, bk,
+                       threads: int = 1) -> np.ndarray:
+        """C = execute(assignment with this [g][2] range table, A, B) of the checker
+        (the reference parses it with its own from_text).  threads = 1 keeps the
+        reference's descending dispatch sequential: safe whenever every fixup wait
+        points to a higher id."""
+        suf = {np.dtype(np.int64): "i64", np.dtype(np.float32): "f32",
+               np.dtype(np.float64): "f64"}[A.dtype]
+        m, k = A.shape
+        n = B.shape[1]
+        A = np.ascontiguousarray(A)
+        B = np.ascontiguousarray(B)
+        ranges = np.ascontiguousarray(ranges, dtype=np.int64).reshape(-1, 2)
+        Cm = np.empty((m, n), A.dtype)
+        fn = ("skor_execute_" if self.kind == "port" else "ref_execute_ranges_") + suf
+        args = [_ptr(ranges), _i64(ranges.shape[0]), _i64(m), _i64(n), _i64(k), _i64(bm), _i64(bn),
+                _i64(bk), _ptr(A), _ptr(B), _ptr(Cm)]
+        if self.kind != "port":
+            args.append(C.c_int(threads))
+        st = getattr(self.lib, fn)(*args)
+        if st:
+            raise OracleError(st, "execute_ranges")
+        return Cm
+
     # ---- reference-only text form -----------------------------------------
     def to_text(self, strategy, m, n, k, bm, bn, bk, param=1) -> str:
         if self.kind != "reference":

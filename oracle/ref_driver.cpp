@@ -77,6 +77,23 @@ int execute_strategy(int strategy, int64_t param, int64_t m, int64_t n, int64_t 
   });
 }
 
+// An arbitrary range table through the reference's own text parser
+// (types.cpp:101-123), then execute<T> (executor.hpp:130-207).
+template <typename T>
+int execute_table(const int64_t* ranges, int64_t g, int64_t m, int64_t n, int64_t k, int64_t bm,
+                  int64_t bn, int64_t bk, const T* A, const T* B, T* C, int threads) {
+  return guarded([&] {
+    std::ostringstream text;
+    text << m << ' ' << n << ' ' << k << '\n' << bm << ' ' << bn << ' ' << bk << '\n'
+         << "stream_k " << g << '\n';
+    for (int64_t i = 0; i < g; ++i) text << i << ' ' << ranges[2 * i] << ' ' << ranges[2 * i + 1] << '\n';
+    const WorkAssignment a = from_text(text.str());
+    const Matrix<T> Am = wrap(A, m, k), Bm = wrap(B, k, n);
+    const Matrix<T> Cm = execute(a, Am, Bm, threads);
+    std::memcpy(C, Cm.data.data(), sizeof(T) * static_cast<size_t>(m * n));
+  });
+}
+
 template <typename T>
 int gemm_ref(int64_t m, int64_t n, int64_t k, int64_t bm, int64_t bn, int64_t bk, const T* A,
              const T* B, T* C) {
@@ -221,6 +238,22 @@ int ref_execute_i64(int strategy, int64_t param, int64_t m, int64_t n, int64_t k
 }
 
 // SKMX files through the reference's own save_matrix/load_matrix (matrix.hpp:78-93).
+int ref_execute_ranges_f32(const int64_t* ranges, int64_t g, int64_t m, int64_t n, int64_t k,
+                           int64_t bm, int64_t bn, int64_t bk, const float* A, const float* B,
+                           float* C, int threads) {
+  return execute_table(ranges, g, m, n, k, bm, bn, bk, A, B, C, threads);
+}
+int ref_execute_ranges_f64(const int64_t* ranges, int64_t g, int64_t m, int64_t n, int64_t k,
+                           int64_t bm, int64_t bn, int64_t bk, const double* A, const double* B,
+                           double* C, int threads) {
+  return execute_table(ranges, g, m, n, k, bm, bn, bk, A, B, C, threads);
+}
+int ref_execute_ranges_i64(const int64_t* ranges, int64_t g, int64_t m, int64_t n, int64_t k,
+                           int64_t bm, int64_t bn, int64_t bk, const int64_t* A, const int64_t* B,
+                           int64_t* C, int threads) {
+  return execute_table(ranges, g, m, n, k, bm, bn, bk, A, B, C, threads);
+}
+
 int ref_save_matrix_f32(const char* path, int64_t r, int64_t c, const float* data) {
   return guarded([&] {
     std::ofstream out(path, std::ios::binary);

@@ -82,7 +82,11 @@ class sk_gemm_desc(C.Structure):
         ("num_ctas", C.c_int32), ("A", C.c_void_p), ("lda", C.c_int64), ("B", C.c_void_p),
         ("ldb", C.c_int64), ("C", C.c_void_p), ("ldc", C.c_int64),
         ("trace", C.c_void_p), ("cta_clocks", C.c_void_p), ("events", C.c_void_p),
+        ("ranges", C.c_void_p), ("num_ranges", C.c_int64),
     ]
+
+
+SK_EXPLICIT = 5  # sk_strategy for an arbitrary range table (skb200.h)
 
 
 _P = C.POINTER
@@ -108,6 +112,11 @@ _SIGS = {
     "sk_gemm": (C.c_int, [_P(sk_gemm_desc), C.c_void_p, C.c_size_t, C.c_void_p]),
     "sk_execute": (C.c_int, [_P(sk_problem), _P(sk_blocking), C.c_int, C.c_int64, C.c_int, C.c_int,
                              C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32]),
+    "sk_execute_ranges": (C.c_int, [_P(sk_problem), _P(sk_blocking), C.c_void_p, C.c_int64, C.c_int,
+                                    C.c_int, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
+                                    C.c_int32]),
+    "sk_fixup_peers_ranges": (C.c_int, [_P(sk_problem), _P(sk_blocking), C.c_void_p, C.c_int64,
+                                        C.c_void_p, C.c_void_p, C.c_int64, _P(C.c_int64)]),
     "sk_execute_release": (None, []),
     "sk_corpus": (C.c_int, [C.c_uint64, C.c_int64, C.c_int64, C.c_int64, C.c_void_p]),
     "sk_default_cost_params": (C.c_int, [C.c_int, C.c_int, C.c_void_p]),
@@ -326,10 +335,32 @@ def fixup_peers_of(a: WorkAssignment) -> List[List[int]]:  # decompose.cpp:123-1
     return [ids[off[t]:off[t + 1]].tolist() for t in range(a.grid.total_tiles)]
 
 
+def _explicit_table(a: WorkAssignment) -> np.ndarray:
+    """The [g][2] range table of an assignment the closed forms do not produce
+    (param == 0), for SK_EXPLICIT.  execute<T> indexes ranges by position while
+    fixup_peers_of keys peers by cta_id (executor.hpp:148, decompose.cpp:130),
+    so a table whose ids differ from their positions has no consistent meaning."""
+    if any(r.cta_id != i for i, r in enumerate(a.ranges)) or len(a.ranges) != a.grid_size:
+        raise ValueError("execute: range table cta_ids must be 0..g-1 in order")
+    return np.ascontiguousarray(a.range_table(), dtype=np.int64)
+
+
 def _peers_csr(a: WorkAssignment):
     p, b = a.problem._c(), a.blocking._c()
     off = np.zeros(a.grid.total_tiles + 1, np.int64)
     nnz = C.c_int64()
+    if a.param == 0:  # explicit table
+        tbl = _explicit_table(a)
+        tp = tbl.ctypes.data_as(C.c_void_p)
+        _check(lib().sk_fixup_peers_ranges(C.byref(p), C.byref(b), tp, tbl.shape[0],
+                                           off.ctypes.data_as(C.c_void_p), None, 0, C.byref(nnz)),
+               "fixup_peers_of")
+        ids = np.zeros(max(nnz.value, 1), np.int64)
+        _check(lib().sk_fixup_peers_ranges(C.byref(p), C.byref(b), tp, tbl.shape[0],
+                                           off.ctypes.data_as(C.c_void_p),
+                                           ids.ctypes.data_as(C.c_void_p), ids.size, C.byref(nnz)),
+               "fixup_peers_of")
+        return off, ids[: nnz.value]
     _check(lib().sk_fixup_peers(C.byref(p), C.byref(b), int(a.strategy), a.param,
                                 off.ctypes.data_as(C.c_void_p), None, 0, C.byref(nnz)),
            "fixup_peers_of")
@@ -557,8 +588,7 @@ def execute(a: WorkAssignment, A: np.ndarray, B: np.ndarray, compute: DType = DT
     p = a.problem
     if A.shape != (p.m, p.k) or B.shape != (p.k, p.n):
         raise ValueError("execute: matrix shapes do not match assignment")
-    if a.param == 0:
-        raise UnsupportedError("execute: range table is not a closed-form schedule")
+    tbl = _explicit_table(a) if a.param == 0 else None  # no closed form: SK_EXPLICIT
     ht = _host_type(A)
     if _host_type(B) != ht:
         raise ValueError("execute: A and B host dtypes differ")
@@ -569,6 +599,13 @@ def execute(a: WorkAssignment, A: np.ndarray, B: np.ndarray, compute: DType = DT
     else:
         cdt = np.float32
     Cm = np.empty((p.m, p.n), cdt)
+    if tbl is not None:
+        _check(lib().sk_execute_ranges(C.byref(p._c()), C.byref(a.blocking._c()),
+                                       tbl.ctypes.data_as(C.c_void_p), tbl.shape[0], int(ht),
+                                       int(compute), int(variant), A.ctypes.data_as(C.c_void_p),
+                                       B.ctypes.data_as(C.c_void_p), Cm.ctypes.data_as(C.c_void_p),
+                                       device), "execute")
+        return Cm
     _check(lib().sk_execute(C.byref(p._c()), C.byref(a.blocking._c()), int(a.strategy), a.param,
                             int(ht), int(compute), int(variant), A.ctypes.data_as(C.c_void_p),
                             B.ctypes.data_as(C.c_void_p), Cm.ctypes.data_as(C.c_void_p), device),
@@ -590,14 +627,18 @@ class Gemm:
                  timeline: bool = False):
         import torch  # device memory only
 
-        if a.param == 0:
-            raise UnsupportedError("Gemm: range table is not a closed-form schedule")
         self.a = a
         self.ab_type = ab_type
         d = sk_gemm_desc()
         d.problem = a.problem._c()
         d.blocking = a.blocking._c()
         d.strategy = int(a.strategy)
+        # a range table no closed form reproduces runs as SK_EXPLICIT
+        self.table = _explicit_table(a) if a.param == 0 else None
+        if self.table is not None:
+            d.strategy = SK_EXPLICIT
+            d.ranges = self.table.ctypes.data
+            d.num_ranges = self.table.shape[0]
         d.ab_type = int(ab_type)
         d.param = a.param
         d.variant = int(variant)

@@ -22,6 +22,11 @@
 //   FS(s)         unit x*s+y  = [x*ipt + min(ipt, y*ips), x*ipt + min(ipt, lo+ips))
 // Peers of any tile are a contiguous id interval [owner, last] (checked
 // exhaustively against fixup_peers_of by tests/test_schedule.py).
+//
+// kExplicit carries an arbitrary range table instead (a WorkAssignment that no
+// closed form produces, e.g. one read back by from_text, types.cpp:109-123):
+// ranges [g][2] and the fixup_peers_of lists in CSR form, validated on the host
+// (one starter per tile at most; a starter's peers all have higher ids).
 #pragma once
 
 #include <stdint.h>
@@ -39,7 +44,8 @@ enum Strategy : int32_t {
   kFixedSplit = 1,
   kStreamK = 2,
   kDpOneTileSk = 3,
-  kTwoTileSkDp = 4
+  kTwoTileSkDp = 4,
+  kExplicit = 5  // range table (not a reference Strategy value; see above)
 };
 
 SK_HD int64_t ceil_div(int64_t x, int64_t y) { return (x + y - 1) / y; }
@@ -89,6 +95,22 @@ struct Schedule {
   int64_t split = 1, ips = 1;
   // fixup slabs: which units emit a partial, compact slab index
   int64_t num_slabs = 0;
+  // kExplicit: [g][2] ranges and per-tile ascending peer ids (CSR); the first
+  // peer of a tile is its starter when that range covers local k = 0.
+  const int64_t* xr = nullptr;
+  const int64_t* xoff = nullptr;
+  const int64_t* xids = nullptr;
+
+  SK_HD int init_explicit(int64_t m_, int64_t n_, int64_t k_, int64_t bm, int64_t bn, int64_t bk,
+                          int64_t g) {
+    if (init(m_, n_, k_, bm, bn, bk, kDataParallel, 1) != 0) return 1;
+    strategy = kExplicit;
+    param = g;
+    grid_size = g;
+    dp_tiles = 0;
+    num_slabs = g;  // slab = unit id (a unit emits at most its first segment)
+    return 0;
+  }
 
   // Returns 0 on success, 1 (EINVAL) on a non-positive extent or parameter.
   SK_HD int init(int64_t m_, int64_t n_, int64_t k_, int64_t bm, int64_t bn, int64_t bk,
@@ -161,6 +183,11 @@ struct Schedule {
 
   // Range of logical CTA u in [0, grid_size).
   SK_HD void range(int64_t u, int64_t* b, int64_t* e) const {
+    if (strategy == kExplicit) {
+      *b = xr[2 * u];
+      *e = xr[2 * u + 1];
+      return;
+    }
     if (strategy == kFixedSplit) {
       const int64_t x = u / split, y = u % split;
       const int64_t lo = imin(ipt, y * ips);
@@ -193,9 +220,28 @@ struct Schedule {
     *last = bal.unit_of((tile + 1) * ipt - 1);
   }
 
+  // Number of peers an owner u of `tile` folds (its covering ranges other than
+  // itself) and the i-th of them, i in [1, npeer], ascending id.
+  SK_HD int npeers(int64_t tile, int64_t u) const {
+    if (strategy == kExplicit) return static_cast<int>(xoff[tile + 1] - xoff[tile] - 1);
+    int64_t owner, last;
+    peers(tile, &owner, &last);
+    return static_cast<int>(last - u);
+  }
+  SK_HD int64_t peer(int64_t tile, int64_t u, int i) const {
+    return strategy == kExplicit ? xids[xoff[tile] + i] : u + i;
+  }
+  // A partial whose tile no range starts is never folded (the reference's
+  // executor leaves that tile of C at zero): explicit tables only.
+  SK_HD bool orphan(int64_t tile) const {
+    if (strategy != kExplicit) return false;
+    return xr[2 * xids[xoff[tile]]] > tile * ipt;
+  }
+
   // Compact slab index of a partial-emitting unit (only units whose first
   // segment starts mid-tile emit; at most one partial per unit).
   SK_HD int64_t slab_of(int64_t u) const {
+    if (strategy == kExplicit) return u;
     if (strategy == kFixedSplit) return (u / split) * (split - 1) + (u % split) - 1;
     return u - bal.first_id;
   }

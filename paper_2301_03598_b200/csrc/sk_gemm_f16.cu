@@ -217,7 +217,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             phase ^= 1;
           }
         }
-      }, P.sk_first != 0);
+      }, P.sk_first);
     }
     __syncwarp();
   } else if (warp == 1) {
@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         else ptx::umma_commit_mc(&tfull_bar[acc], 0x3);
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
-      }, P.sk_first != 0);
+      }, P.sk_first);
     }
     __syncwarp();
   } else {
@@ -281,12 +281,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const int32_t m0 = static_cast<int32_t>((tile / s.tiles_n) * (ROWS * CG) + rank * ROWS);
       const int32_t n0 = static_cast<int32_t>((tile % s.tiles_n) * BN);
       const bool partial = lb != 0;  // not the tile starter (executor.hpp:160)
-      int64_t owner = u, last = u;
-      if (!partial && le < s.ipt) s.peers(tile, &owner, &last);
-      const int npeer = static_cast<int>(last - u);
+      const bool orphan = partial && s.orphan(tile);  // explicit table: nobody folds it
+      const int npeer = (!partial && (le < s.ipt || s.strategy == kExplicit)) ? s.npeers(tile, u) : 0;
       if (npeer > 0) {
         if (lane == 0)
-          for (int p = 1; p <= npeer; ++p) wait_flag(P, P.flags + fidx(u + p));
+          for (int p = 1; p <= npeer; ++p) wait_flag(P, P.flags + fidx(s.peer(tile, u, p)));
         __syncwarp();
       }
       if (ev) ev[kEvWaitEnd] = ptx::globaltimer();
@@ -295,7 +294,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       // of peer slab in flight per thread, two 32x32 TMA-store boxes.
       const int c_lo = static_cast<int>((warp - 2) / 4) * (EPI_COLS / 32);
 #pragma unroll 1
-      for (int c = c_lo; c < c_lo + EPI_COLS / 32; c += 2) {
+      for (int c = c_lo; c < (orphan ? c_lo : c_lo + EPI_COLS / 32); c += 2) {
         float v[64];
         ptx::tmem_ld64(tsrc + c * 32, v);
         if (partial) {
@@ -307,7 +306,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           // Owner fold: own accumulator, then peers in ascending id (executor.hpp:165-172).
 #pragma unroll 1
           for (int p = 1; p <= npeer; ++p) {
-            float* ps = partials + fidx(u + p) * static_cast<int64_t>(SLAB_ELEMS);
+            float* ps = partials + fidx(s.peer(tile, u, p)) * static_cast<int64_t>(SLAB_ELEMS);
             float4 w[16];
 #pragma unroll
             for (int j = 0; j < 16; ++j) w[j] = ptx::ld_cg_f4(slab_ptr(ps, c + j / 8, j % 8, row));
@@ -361,23 +360,23 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if constexpr (CG == 1) ptx::mbar_arrive(&tempty_bar[acc]);
         else mbar_arrive_remote(mapa(&tempty_bar[acc], 0));
       }
-      if (partial) {
+      if (partial && !orphan) {
         __threadfence();
         ptx::named_bar_sync(1, 32 * EPI_WARPS);
         if (leader) {
           signal_flag(P, P.flags + fidx(u));
           if (P.trace && rank == 0) atomicAdd(P.trace + 4 * s.total_tiles + u, 1);
         }
-      } else {
+      } else if (!partial) {
         if (npeer > 0) {
           ptx::named_bar_sync(1, 32 * EPI_WARPS);
           if (leader)  // every epilogue warp has read the slabs: re-arm the flags
-            for (int p = 1; p <= npeer; ++p) ptx::st_relaxed(P.flags + fidx(u + p), 0);
+            for (int p = 1; p <= npeer; ++p) ptx::st_relaxed(P.flags + fidx(s.peer(tile, u, p)), 0);
         }
         if (leader && P.trace && rank == 0) {
           int* t = P.trace + 4 * tile;
-          t[0] = static_cast<int>(owner);
-          t[1] = static_cast<int>(last);
+          t[0] = static_cast<int>(u);
+          t[1] = static_cast<int>(s.peer(tile, u, npeer));
           t[2] = static_cast<int>(u);
           t[3] = npeer;
         }
@@ -386,12 +385,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         ev[kEvUnit] = u;
         ev[kEvTile] = tile;
         ev[kEvCore] = cta;
-        ev[kEvKind] = (partial ? 1 : 0) | (npeer > 0 ? 2 : 0) | (static_cast<long long>(npeer) << 8);
+        ev[kEvKind] = (partial ? 1 : 0) | (npeer > 0 ? 2 : 0) | (static_cast<long long>(npeer) << 8) |
+                      (static_cast<long long>(ptx::smid()) << 16);
         ev[kEvDone] = ptx::globaltimer();
       }
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
-    }, P.sk_first != 0);
+    }, P.sk_first);
     if (lane == 0) ptx::tma_store_wait_all<0>();
     __syncwarp();
   }

@@ -112,7 +112,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
             phase ^= 1;
           }
         }
-      }, P.sk_first != 0);
+      }, P.sk_first);
     }
     return;
   }
@@ -166,15 +166,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
     }
 
     const bool partial = lb != 0;
-    int64_t owner = u, last = u;
-    if (!partial && le < s.ipt) s.peers(tile, &owner, &last);
-    const int npeer = static_cast<int>(last - u);
+    const int npeer = (!partial && (le < s.ipt || s.strategy == kExplicit)) ? s.npeers(tile, u) : 0;
     if (ev) {
       ev[kEvMacEnd] = ptx::globaltimer();
       ev[kEvUnit] = u;
       ev[kEvTile] = tile;
       ev[kEvCore] = cta;
-      ev[kEvKind] = (partial ? 1 : 0) | (npeer > 0 ? 2 : 0) | (static_cast<long long>(npeer) << 8);
+      ev[kEvKind] = (partial ? 1 : 0) | (npeer > 0 ? 2 : 0) | (static_cast<long long>(npeer) << 8) |
+                      (static_cast<long long>(ptx::smid()) << 16);
+    }
+    if (partial && s.orphan(tile)) {  // explicit table: no range starts this tile
+      if (ev) ev[kEvWaitEnd] = ev[kEvDone] = ptx::globaltimer();
+      return;
     }
     if (partial) {
       double* slab = partials + s.slab_of(u) * static_cast<int64_t>(SLAB_ELEMS);
@@ -195,12 +198,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
     }
     if (npeer > 0) {
       if (tid == 0)
-        for (int p = 1; p <= npeer; ++p) wait_flag(P, P.flags + s.slab_of(u + p));
+        for (int p = 1; p <= npeer; ++p) wait_flag(P, P.flags + s.slab_of(s.peer(tile, u, p)));
       ptx::named_bar_sync(1, 128);
       if (ev) ev[kEvWaitEnd] = ptx::globaltimer();
       // Owner fold: own accumulator, then peers in ascending id (executor.hpp:165-172).
       for (int p = 1; p <= npeer; ++p) {
-        const double* slab = partials + s.slab_of(u + p) * static_cast<int64_t>(SLAB_ELEMS);
+        const double* slab = partials + s.slab_of(s.peer(tile, u, p)) * static_cast<int64_t>(SLAB_ELEMS);
 #pragma unroll
         for (int i = 0; i < 2; ++i)
 #pragma unroll
@@ -210,12 +213,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
       }
       ptx::named_bar_sync(1, 128);
       if (tid == 0)
-        for (int p = 1; p <= npeer; ++p) ptx::st_relaxed(P.flags + s.slab_of(u + p), 0);
+        for (int p = 1; p <= npeer; ++p) ptx::st_relaxed(P.flags + s.slab_of(s.peer(tile, u, p)), 0);
     }
     if (tid == 0 && P.trace) {
       int* t = P.trace + 4 * tile;
-      t[0] = static_cast<int>(owner);
-      t[1] = static_cast<int>(last);
+      t[0] = static_cast<int>(u);
+      t[1] = static_cast<int>(s.peer(tile, u, npeer));
       t[2] = static_cast<int>(u);
       t[3] = npeer;
     }
@@ -241,7 +244,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
       if (npeer == 0) ev[kEvWaitEnd] = ev[kEvMacEnd];
       ev[kEvDone] = ptx::globaltimer();
     }
-  }, P.sk_first != 0);
+  }, P.sk_first);
   stamp_clock(P, 1);
 #endif
 }

@@ -14,14 +14,17 @@ namespace skb200 {
 //   [0, 256)                   header: int err word (+ reserved)
 //   [256, 256 + flag_bytes)    int32 flags, one per (slab, cta rank), zero between launches
 //   [partials_off, ...)        fixup slabs: num_slabs * ranks * slab_elems accumulators
+//   [table_off, total)         explicit schedules only: ranges, peer offsets, peer ids (int64)
 struct WorkspaceLayout {
-  size_t flags_off = 256, flag_bytes = 0, partials_off = 0, total = 0;
+  size_t flags_off = 256, flag_bytes = 0, partials_off = 0, table_off = 0, total = 0;
   static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
-  void compute(int64_t num_slabs, int ranks, size_t slab_bytes) {
+  void compute(int64_t num_slabs, int ranks, size_t slab_bytes, size_t table_bytes = 0) {
     flags_off = 256;
     flag_bytes = align256(sizeof(int) * static_cast<size_t>(num_slabs * ranks + 1));
     partials_off = flags_off + flag_bytes;
-    total = partials_off + static_cast<size_t>(num_slabs * ranks) * slab_bytes;
+    table_off = align256(partials_off + static_cast<size_t>(num_slabs * ranks) * slab_bytes);
+    total = table_bytes ? table_off + table_bytes
+                        : partials_off + static_cast<size_t>(num_slabs * ranks) * slab_bytes;
   }
 };
 
@@ -44,7 +47,7 @@ struct KernelParams {
   int64_t seg_stride;     // max tile segments of one unit (timeline indexing)
   int64_t watchdog_ns;
   int64_t raster_rows;  // data-parallel tile-row group height (1 = row-major)
-  int32_t sk_first;      // TwoTileSkDp: run the SK region before the DP waves
+  int32_t sk_first;      // TwoTileSkDp phase order: kDpFirst, kSkFirst, kInterleaved
   int32_t l2_policy[4];  // L2 eviction priority for A loads, B loads (data-parallel
                          // units), C stores, B loads (Stream-K / fixed-split units):
                          // 0 normal, 1 evict_first, 2 evict_last
@@ -95,20 +98,39 @@ __device__ __forceinline__ void run_unit(const Schedule& s, int64_t u, F& f) {
   }
 }
 
+// Phase orders for TwoTileSkDp (KernelParams::sk_first):
+enum : int { kDpFirst = 0, kSkFirst = 1, kInterleaved = 2 };
+
 template <class F>
 __device__ __forceinline__ void for_each_segment(const Schedule& s, int64_t cta, int64_t P,
-                                                 int64_t raster_rows, F&& f, bool sk_first = false) {
+                                                 int64_t raster_rows, F&& f, int order = kDpFirst) {
   auto dp_phase = [&] {
     for (int64_t i = cta; i < s.dp_tiles; i += P) run_unit(s, s.dp_id0 + raster_tile(s, i, raster_rows), f);
   };
   auto desc_phase = [&](int64_t lo, int64_t hi) {
     for (int64_t u = hi - 1 - cta; u >= lo; u -= P) run_unit(s, u, f);
   };
-  if (s.strategy == kFixedSplit) {
+  if (s.strategy == kFixedSplit || s.strategy == kExplicit) {
     desc_phase(0, s.grid_size);
   } else if (s.bal.count == 0) {
     dp_phase();
-  } else if (s.dp_id0 > s.bal.first_id && !sk_first) {  // TwoTileSkDp, DP wave(s) first
+  } else if (s.dp_id0 > s.bal.first_id && order == kInterleaved && s.bal.count <= P) {
+    // TwoTileSkDp with at most one balanced unit per CTA, staggered through the
+    // data-parallel waves: CTA `cta` runs unit hi-1-cta after `slot` of its own
+    // data-parallel tiles, slot rising with cta.  A tile's peers (higher ids =
+    // lower cta) therefore run no later than its owner, and at any moment only
+    // ~1/(waves+1) of the CTAs are in the bandwidth-heavy balanced region.
+    const int64_t hi = s.bal.first_id + s.bal.count;
+    const int64_t u = hi - 1 - cta;
+    const int64_t waves = (s.dp_tiles + P - 1) / P;
+    const int64_t slot = u >= s.bal.first_id ? cta * (waves + 1) / P : -1;
+    int64_t j = 0;
+    for (int64_t i = cta; i < s.dp_tiles; i += P, ++j) {
+      if (j == slot) run_unit(s, u, f);
+      run_unit(s, s.dp_id0 + raster_tile(s, i, raster_rows), f);
+    }
+    if (slot >= j) run_unit(s, u, f);
+  } else if (s.dp_id0 > s.bal.first_id && order == kDpFirst) {  // TwoTileSkDp, DP wave(s) first
     dp_phase();
     desc_phase(s.bal.first_id, s.bal.first_id + s.bal.count);
   } else {  // StreamK, DpOneTileSk, TwoTileSkDp with the SK region first (Fig. 4c)
@@ -129,7 +151,8 @@ __device__ __forceinline__ void stamp_clock(const KernelParams& P, int slot) {
 
 // Device timeline (sk_gemm_desc.events): one record per (unit, tile segment)
 //   {unit, tile, core, kind, t_mac_start, t_mac_end, t_wait_end, t_done}
-// with kind = 1 partial | 2 owner-with-peers | npeer << 8, times in globaltimer ns.
+// with kind = 1 partial | 2 owner-with-peers | npeer << 8 | smid << 16, times in
+// globaltimer ns.
 // Rendered as the reference's timeline CSV / Gantt (simulate.cpp:105-168).
 enum { kEvUnit = 0, kEvTile, kEvCore, kEvKind, kEvMacStart, kEvMacEnd, kEvWaitEnd, kEvDone };
 __device__ __forceinline__ long long* event_slot(const KernelParams& P, int64_t u, int64_t tile) {

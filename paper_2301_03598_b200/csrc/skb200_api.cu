@@ -135,6 +135,7 @@ sk_status make_tmap(CUtensorMap* m, CUtensorMapDataType dt, size_t esize, const 
 // flag region only when it overlaps that hull.
 struct Dirty {
   size_t lo = 0, hi = 0;  // [lo, hi), empty when lo >= hi
+  uint64_t table = 0;     // hash of the explicit table the workspace tail holds (0 = none)
 };
 std::mutex g_ws_mu;
 std::unordered_map<const void*, Dirty> g_ws_dirty;
@@ -148,11 +149,16 @@ void ws_mark_all_dirty(const void* ws) {
   g_ws_dirty[ws] = Dirty{0, ~size_t(0)};
 }
 // Returns true when [flags_off, flags_end) must be zeroed before this launch.
-bool ws_prepare(const void* ws, size_t flags_off, size_t flags_end, size_t slabs_end) {
+// *upload: whether an explicit table (hash `table`, 0 = closed form) must be
+// copied into the workspace tail; any other launch invalidates a resident table.
+bool ws_prepare(const void* ws, size_t flags_off, size_t flags_end, size_t slabs_end,
+                uint64_t table = 0, bool* upload = nullptr) {
   std::lock_guard<std::mutex> lk(g_ws_mu);
   auto it = g_ws_dirty.find(ws);
   bool clear = false;
   Dirty d = it == g_ws_dirty.end() ? Dirty{} : it->second;
+  if (upload) *upload = table != 0 && d.table != table;
+  d.table = table;
   if (d.lo < d.hi && d.lo < flags_end && flags_off < d.hi) {
     clear = true;
     if (d.lo < flags_end) d.lo = flags_end;
@@ -182,6 +188,83 @@ sk_status init_schedule(const sk_problem* p, const sk_blocking* b, int32_t strat
       return fail(SK_EINVAL, "BlockingFactors must be >= 1");
     return fail(SK_EINVAL, "strategy parameter must be >= 1");
   }
+  return SK_OK;
+}
+
+// ---- explicit range tables (SK_EXPLICIT) ---------------------------------------
+// Host copy of a validated table: ranges, then fixup_peers_of (decompose.cpp:123-136)
+// as CSR, laid out exactly as it is copied into the workspace tail.
+struct ExplicitTable {
+  std::vector<int64_t> data;  // [2g ranges][t + 1 offsets][nnz ids]
+  int64_t g = 0, tiles = 0, nnz = 0;
+  bool all_started = true;
+  uint64_t hash = 0;
+  const int64_t* ranges() const { return data.data(); }
+  const int64_t* off() const { return data.data() + 2 * g; }
+  const int64_t* ids() const { return data.data() + 2 * g + tiles + 1; }
+  size_t bytes() const { return data.size() * sizeof(int64_t); }
+};
+thread_local ExplicitTable g_xt;
+
+// Bounds (mac_loop's contract, executor.hpp:63-68) and peer lists; with
+// `protocol`, also the two conditions the persistent grid needs (see skb200.h).
+sk_status build_explicit(const Schedule& s, const int64_t* r, int64_t g, bool protocol,
+                         ExplicitTable* x) {
+  if (g < 0) return fail(SK_EINVAL, "num_ranges < 0");
+  if (g > 0 && !r) return fail(SK_EINVAL, "null range table");
+  const int64_t t = s.total_tiles, ipt = s.ipt;
+  std::vector<int64_t> cnt(static_cast<size_t>(t + 1), 0);
+  for (int64_t u = 0; u < g; ++u) {
+    const int64_t b = r[2 * u], e = r[2 * u + 1];
+    if (b < 0 || e < b || e > s.total_iters)
+      return fail(SK_EINVAL, "range %lld [%lld, %lld) outside [0, %lld)", (long long)u,
+                  (long long)b, (long long)e, (long long)s.total_iters);
+    if (b == e) continue;  // empty ranges are nobody's peer (decompose.cpp:127)
+    for (int64_t tile = b / ipt; tile <= (e - 1) / ipt; ++tile) ++cnt[static_cast<size_t>(tile + 1)];
+  }
+  for (int64_t i = 0; i < t; ++i) cnt[static_cast<size_t>(i + 1)] += cnt[static_cast<size_t>(i)];
+  x->g = g;
+  x->tiles = t;
+  x->nnz = cnt[static_cast<size_t>(t)];
+  x->data.assign(static_cast<size_t>(2 * g + t + 1 + x->nnz), 0);
+  std::copy(r, r + 2 * g, x->data.begin());
+  int64_t* off = x->data.data() + 2 * g;
+  int64_t* ids = off + t + 1;
+  std::copy(cnt.begin(), cnt.end(), off);
+  std::vector<int64_t> fill(cnt.begin(), cnt.end() - 1);
+  for (int64_t u = 0; u < g; ++u) {  // ascending u: every list comes out sorted
+    const int64_t b = r[2 * u], e = r[2 * u + 1];
+    if (b == e) continue;
+    for (int64_t tile = b / ipt; tile <= (e - 1) / ipt; ++tile) ids[fill[static_cast<size_t>(tile)]++] = u;
+  }
+  x->all_started = true;
+  for (int64_t tile = 0; tile < t; ++tile) {
+    int64_t starter = -1;
+    for (int64_t q = off[tile]; q < off[tile + 1]; ++q) {
+      const int64_t u = ids[q];
+      if (r[2 * u] > tile * ipt) continue;  // joins mid-tile: a partial
+      if (protocol && starter >= 0)
+        return fail(SK_EINVAL, "tile %lld is started by ranges %lld and %lld (the reference "
+                    "executor would wait on both forever)", (long long)tile, (long long)starter,
+                    (long long)u);
+      starter = u;
+    }
+    if (starter < 0) {
+      x->all_started = false;
+    } else if (protocol && starter != ids[off[tile]]) {
+      return fail(SK_EUNSUPPORTED, "tile %lld: starter %lld would wait on lower id %lld; only "
+                  "tables whose fixup waits point to higher ids run on a persistent grid",
+                  (long long)tile, (long long)starter, (long long)ids[off[tile]]);
+    }
+  }
+  uint64_t h = 1469598103934665603ull;  // FNV-1a over the table and the tile grid
+  auto mix = [&](uint64_t v) {
+    for (int i = 0; i < 8; ++i) h = (h ^ ((v >> (8 * i)) & 0xff)) * 1099511628211ull;
+  };
+  mix(static_cast<uint64_t>(ipt));
+  mix(static_cast<uint64_t>(t));
+  for (int64_t v : x->data) mix(static_cast<uint64_t>(v));
+  x->hash = h ? h : 1;
   return SK_OK;
 }
 
@@ -243,8 +326,20 @@ size_t kernel_slab_bytes(Kernel k) {
 
 sk_status check_desc(const sk_gemm_desc* d, Kernel* kern, Schedule* s) {
   if (!d) return fail(SK_EINVAL, "null descriptor");
-  sk_status st = init_schedule(&d->problem, &d->blocking, d->strategy, d->param, s);
-  if (st) return st;
+  sk_status st;
+  if (d->strategy == SK_EXPLICIT) {
+    if (s->init_explicit(d->problem.m, d->problem.n, d->problem.k, d->blocking.blk_m,
+                         d->blocking.blk_n, d->blocking.blk_k, d->num_ranges) != 0)
+      return init_schedule(&d->problem, &d->blocking, SK_DATA_PARALLEL, 1, s);  // the message
+    st = build_explicit(*s, d->ranges, d->num_ranges, true, &g_xt);
+    if (st) return st;
+    s->xr = g_xt.ranges();
+    s->xoff = g_xt.off();
+    s->xids = g_xt.ids();
+  } else {
+    st = init_schedule(&d->problem, &d->blocking, d->strategy, d->param, s);
+    if (st) return st;
+  }
   st = pick_kernel(d, kern);
   if (st) return st;
   sk_blocking kb;
@@ -341,6 +436,25 @@ sk_status sk_fixup_peers(const sk_problem* p, const sk_blocking* b, sk_strategy 
   return SK_OK;
 }
 
+sk_status sk_fixup_peers_ranges(const sk_problem* p, const sk_blocking* b, const int64_t* ranges,
+                                int64_t num_ranges, int64_t* offsets, int64_t* ids,
+                                int64_t capacity, int64_t* nnz) {
+  if (!p || !b) return fail(SK_EINVAL, "null problem/blocking");
+  Schedule s;
+  if (s.init_explicit(p->m, p->n, p->k, b->blk_m, b->blk_n, b->blk_k, num_ranges) != 0)
+    return init_schedule(p, b, SK_DATA_PARALLEL, 1, &s);
+  if (!offsets) return fail(SK_EINVAL, "null offsets");
+  ExplicitTable x;
+  sk_status st = build_explicit(s, ranges, num_ranges, false, &x);
+  if (st) return st;
+  std::copy(x.off(), x.off() + x.tiles + 1, offsets);
+  if (nnz) *nnz = x.nnz;
+  if (!ids) return SK_OK;
+  if (capacity < x.nnz) return fail(SK_ECAPACITY, "ids capacity too small");
+  std::copy(x.ids(), x.ids() + x.nnz, ids);
+  return SK_OK;
+}
+
 sk_status sk_quantization_efficiency(int64_t t, int64_t p, double* out) {
   if (t < 1 || p < 1) return fail(SK_EINVAL, "quantization_efficiency: t, p >= 1");
   if (out) *out = static_cast<double>(t) / static_cast<double>(ceil_div(t, p) * p);
@@ -389,7 +503,8 @@ sk_status sk_workspace_size(const sk_gemm_desc* d, size_t* bytes) {
   sk_status st = check_desc(d, &k, &s);
   if (st) return st;
   WorkspaceLayout L;
-  L.compute(s.num_slabs, kernel_ranks(k), kernel_slab_bytes(k));
+  L.compute(s.num_slabs, kernel_ranks(k), kernel_slab_bytes(k),
+            s.strategy == kExplicit ? g_xt.bytes() : 0);
   if (bytes) *bytes = L.total;
   return SK_OK;
 }
@@ -462,8 +577,9 @@ sk_status sk_gemm(const sk_gemm_desc* d, void* ws, size_t ws_bytes, void* stream
     return fail(SK_EUNSUPPORTED, "matrix base pointers must be 16-byte aligned");
   if ((d->lda * esz) % 16 || (d->ldb * esz) % 16 || (d->ldc * csz) % 16)
     return fail(SK_EUNSUPPORTED, "leading dimensions must be multiples of 16 bytes (TMA)");
+  const bool xp = s.strategy == kExplicit;
   WorkspaceLayout L;
-  L.compute(s.num_slabs, kernel_ranks(kern), kernel_slab_bytes(kern));
+  L.compute(s.num_slabs, kernel_ranks(kern), kernel_slab_bytes(kern), xp ? g_xt.bytes() : 0);
   if (!ws || ws_bytes < L.total)
     return fail(SK_EINVAL, "workspace of %zu bytes < required %zu", ws_bytes, L.total);
 
@@ -476,11 +592,19 @@ sk_status sk_gemm(const sk_gemm_desc* d, void* ws, size_t ws_bytes, void* stream
     return fail(SK_EUNSUPPORTED, "device sm_%d%d: this build targets sm_100a only", info.cc_major,
                 info.cc_minor);
   cudaStream_t strm = static_cast<cudaStream_t>(stream);
-  if (ws_prepare(ws, L.flags_off, L.partials_off, L.total))
+  bool upload = false;
+  if (ws_prepare(ws, L.flags_off, L.partials_off, L.total, xp ? g_xt.hash : 0, &upload))
     SK_CUDA(cudaMemsetAsync(static_cast<uint8_t*>(ws) + L.flags_off, 0, L.flag_bytes, strm));
 
   KernelParams P{};
   P.s = s;
+  if (xp) {  // the kernel reads the table from the workspace tail
+    int64_t* tb = reinterpret_cast<int64_t*>(static_cast<uint8_t*>(ws) + L.table_off);
+    if (upload) SK_CUDA(cudaMemcpyAsync(tb, g_xt.data.data(), g_xt.bytes(), cudaMemcpyHostToDevice, strm));
+    P.s.xr = tb;
+    P.s.xoff = tb + 2 * g_xt.g;
+    P.s.xids = tb + 2 * g_xt.g + g_xt.tiles + 1;
+  }
   P.ranks = kernel_ranks(kern);
   uint8_t* wsb = static_cast<uint8_t*>(ws);
   P.err = reinterpret_cast<int*>(wsb);
@@ -613,10 +737,11 @@ int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
 }  // namespace
 
-extern "C" sk_status sk_execute(const sk_problem* p, const sk_blocking* b, sk_strategy strategy,
-                                int64_t param, sk_dtype host_type, sk_dtype compute_type,
-                                int32_t variant, const void* A, const void* B, void* C,
-                                int32_t device) {
+namespace {
+sk_status execute_impl(const sk_problem* p, const sk_blocking* b, sk_strategy strategy,
+                       int64_t param, const int64_t* ranges, int64_t num_ranges,
+                       sk_dtype host_type, sk_dtype compute_type, int32_t variant, const void* A,
+                       const void* B, void* C, int32_t device) {
   if (!p || !b || !A || !B || !C) return fail(SK_EINVAL, "null argument");
   if (compute_type != SK_BFLOAT16 && compute_type != SK_FLOAT16 && compute_type != SK_FLOAT64)
     return fail(SK_EUNSUPPORTED, "compute_type %d has no device kernel", compute_type);
@@ -640,17 +765,6 @@ extern "C" sk_status sk_execute(const sk_problem* p, const sk_blocking* b, sk_st
       return fail(SK_EUNSUPPORTED, "int64 operands exceed the exact fp64 range (max|A|max|B|k >= 2^53)");
   }
 
-  int dev = device;
-  if (dev < 0) SK_CUDA(cudaGetDevice(&dev));
-  ExecCache& X = g_exec;
-  if (X.device != dev) {
-    X.release();
-    SK_CUDA(cudaSetDevice(dev));
-    SK_CUDA(cudaStreamCreateWithFlags(&X.stream, cudaStreamNonBlocking));
-    X.device = dev;
-  } else {
-    SK_CUDA(cudaSetDevice(dev));
-  }
   const int64_t m = p->m, n = p->n, k = p->k;
   if (m < 1 || n < 1 || k < 1) return fail(SK_EINVAL, "GemmProblem extents must be >= 1");
   const size_t esz = dtype_size(compute_type), csz = is16 ? 4 : 8;
@@ -669,9 +783,25 @@ extern "C" sk_status sk_execute(const sk_problem* p, const sk_blocking* b, sk_st
   d.lda = lda;
   d.ldb = ldb;
   d.ldc = ldc;
+  d.ranges = ranges;
+  d.num_ranges = num_ranges;
   size_t ws_bytes = 0;
   sk_status st = sk_workspace_size(&d, &ws_bytes);
   if (st) return st;
+  // A fresh C is zero (matrix.hpp:22): only explicit tables can leave tiles unwritten.
+  const bool zero_c = strategy == SK_EXPLICIT && !g_xt.all_started;
+
+  int dev = device;
+  if (dev < 0) SK_CUDA(cudaGetDevice(&dev));
+  ExecCache& X = g_exec;
+  if (X.device != dev) {
+    X.release();
+    SK_CUDA(cudaSetDevice(dev));
+    SK_CUDA(cudaStreamCreateWithFlags(&X.stream, cudaStreamNonBlocking));
+    X.device = dev;
+  } else {
+    SK_CUDA(cudaSetDevice(dev));
+  }
 
   st = X.ensure(0, static_cast<size_t>(m * lda) * esz);
   if (!st) st = X.ensure(1, static_cast<size_t>(k * ldb) * esz);
@@ -710,6 +840,7 @@ extern "C" sk_status sk_execute(const sk_problem* p, const sk_blocking* b, sk_st
   d.A = X.buf[0];
   d.B = X.buf[1];
   d.C = X.buf[2];
+  if (zero_c) SK_CUDA(cudaMemsetAsync(X.buf[2], 0, static_cast<size_t>(m * ldc) * csz, s));
   st = sk_gemm(&d, X.buf[3], ws_bytes, s);
   if (st) return st;
   if (!is16 && host_type != SK_FLOAT64) {
@@ -721,6 +852,24 @@ extern "C" sk_status sk_execute(const sk_problem* p, const sk_blocking* b, sk_st
     SK_CUDA(cudaMemcpy2DAsync(C, n * csz, X.buf[2], ldc * csz, n * csz, m, cudaMemcpyDeviceToHost, s));
   }
   return sk_workspace_check(X.buf[3], s);
+}
+}  // namespace
+
+extern "C" sk_status sk_execute(const sk_problem* p, const sk_blocking* b, sk_strategy strategy,
+                                int64_t param, sk_dtype host_type, sk_dtype compute_type,
+                                int32_t variant, const void* A, const void* B, void* C,
+                                int32_t device) {
+  if (strategy == SK_EXPLICIT) return fail(SK_EINVAL, "SK_EXPLICIT: use sk_execute_ranges");
+  return execute_impl(p, b, strategy, param, nullptr, 0, host_type, compute_type, variant, A, B,
+                      C, device);
+}
+
+extern "C" sk_status sk_execute_ranges(const sk_problem* p, const sk_blocking* b,
+                                       const int64_t* ranges, int64_t num_ranges,
+                                       sk_dtype host_type, sk_dtype compute_type, int32_t variant,
+                                       const void* A, const void* B, void* C, int32_t device) {
+  return execute_impl(p, b, SK_EXPLICIT, num_ranges, ranges, num_ranges, host_type, compute_type,
+                      variant, A, B, C, device);
 }
 
 extern "C" void sk_execute_release(void) { g_exec.release(); }

@@ -11,6 +11,8 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <algorithm>
+#include <sstream>
 #include <vector>
 
 #include "streamk/decompose.hpp"
@@ -130,6 +132,79 @@ std::string execute_float_double() {
   return "";
 }
 
+// A table no closed form produces, through the reference's own text parser
+// (types.cpp:101-123): random monotone cuts over [0, total), some ranges empty.
+WorkAssignment random_table(Rng& rng, const GemmProblem& p, const BlockingFactors& b) {
+  const TileGrid g = tile_grid(p, b);
+  const int64_t n = rng.uniform(1, 3 * g.total_tiles + 2);
+  std::vector<int64_t> cuts(static_cast<size_t>(n - 1));
+  for (auto& c : cuts) c = rng.uniform(0, g.total_iters);
+  std::sort(cuts.begin(), cuts.end());
+  std::ostringstream text;
+  text << p.m << ' ' << p.n << ' ' << p.k << '\n' << b.blk_m << ' ' << b.blk_n << ' ' << b.blk_k
+       << "\nstream_k " << n << '\n';
+  int64_t prev = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    const int64_t e = i + 1 < n ? cuts[static_cast<size_t>(i)] : g.total_iters;
+    const bool drop = rng.uniform(0, 4) == 0;
+    text << i << ' ' << prev << ' ' << (drop ? prev : e) << '\n';
+    prev = e;
+  }
+  return from_text(text.str());
+}
+
+std::string explicit_peers() {
+  Rng rng(0x7ab1e5ULL);
+  for (int trial = 0; trial < 500; ++trial) {
+    const GemmProblem p = random_problem(rng, 300);
+    const BlockingFactors b = random_blocking(rng, 40);
+    const WorkAssignment a = random_table(rng, p, b);
+    const sk_problem pr = streamk_b200::to_sk(a.problem);
+    const sk_blocking bl = streamk_b200::to_sk(a.blocking);
+    std::vector<int64_t> tbl;
+    for (const CtaRange& r : a.ranges) {
+      tbl.push_back(r.iter_begin);
+      tbl.push_back(r.iter_end);
+    }
+    const auto peers = fixup_peers_of(a);
+    std::vector<int64_t> off(peers.size() + 1);
+    int64_t nnz = 0;
+    if (sk_fixup_peers_ranges(&pr, &bl, tbl.data(), a.grid_size, off.data(), nullptr, 0, &nnz) != SK_OK)
+      return "sk_fixup_peers_ranges failed";
+    std::vector<int64_t> ids(static_cast<size_t>(std::max<int64_t>(nnz, 1)));
+    sk_fixup_peers_ranges(&pr, &bl, tbl.data(), a.grid_size, off.data(), ids.data(), nnz, &nnz);
+    for (size_t t = 0; t < peers.size(); ++t) {
+      if (static_cast<size_t>(off[t + 1] - off[t]) != peers[t].size()) return "peer count";
+      for (size_t q = 0; q < peers[t].size(); ++q)
+        if (ids[static_cast<size_t>(off[t]) + q] != peers[t][q]) return "peer ids";
+    }
+  }
+  return "";
+}
+
+std::string execute_explicit() {
+  Rng rng(0xe4b1c17ULL);
+  for (int trial = 0; trial < 8; ++trial) {
+    const GemmProblem p{rng.uniform(1, 600), rng.uniform(1, 600), rng.uniform(1, 700)};
+    const BlockingFactors b = trial % 2 ? BlockingFactors{64, 64, 16} : BlockingFactors{256, 256, 64};
+    const WorkAssignment a = random_table(rng, p, b);
+    const auto Ai = random_matrix<std::int64_t>(p.m, p.k, 50 + trial);
+    const auto Bi = random_matrix<std::int64_t>(p.k, p.n, 51 + trial);
+    const auto want = execute(a, Ai, Bi, 1);
+    if (trial % 2) {
+      if (streamk_b200::execute(a, Ai, Bi).data != want.data) return "int64 explicit table (DMMA)";
+    } else {
+      Matrix<float> A(p.m, p.k), B(p.k, p.n);
+      for (size_t i = 0; i < A.data.size(); ++i) A.data[i] = static_cast<float>(Ai.data[i]);
+      for (size_t i = 0; i < B.data.size(); ++i) B.data[i] = static_cast<float>(Bi.data[i]);
+      const auto got = streamk_b200::execute(a, A, B, streamk_b200::Precision::BF16);
+      for (size_t i = 0; i < got.data.size(); ++i)
+        if (got.data[i] != static_cast<float>(want.data[i])) return "bf16 explicit table (tcgen05)";
+    }
+  }
+  return "";
+}
+
 std::string errors_map_to_reference_exceptions() {
   const GemmProblem p{64, 64, 64};
   Matrix<double> A(64, 63), B(64, 64);
@@ -150,12 +225,15 @@ int main(int argc, char** argv) {
     report("sk_schedule / sk_fixup_peers == decompose.cpp (3000 instances x 5 strategies)",
            schedule_parity());
     report("shape errors -> std::invalid_argument", errors_map_to_reference_exceptions());
+    report("sk_fixup_peers_ranges == fixup_peers_of on from_text tables (500)", explicit_peers());
   }
   if (exec) {
     report("execute<int64_t>: bit-exact vs naive and streamk::execute (60 instances x 5)",
            execute_int64());
     report("execute<float>/<double> under 8 eps k; bf16 path exact on the int band",
            execute_float_double());
+    report("execute on from_text tables (SK_EXPLICIT) == streamk::execute, bit-exact (8)",
+           execute_explicit());
   }
   return failures ? 1 : 0;
 }

@@ -21,11 +21,11 @@ def _binary():
 def test_cpp_shim_schedule(sk):
     out = subprocess.run([_binary(), "--schedule"], capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stdout + out.stderr
-    assert out.stdout.count("[PASS]") == 2
+    assert out.stdout.count("[PASS]") == 3
 
 
 @pytest.mark.gpu
 def test_cpp_shim_execute(sk):
     out = subprocess.run([_binary(), "--execute"], capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stdout + out.stderr
-    assert out.stdout.count("[PASS]") == 2
+    assert out.stdout.count("[PASS]") == 3
