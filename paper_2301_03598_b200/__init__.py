@@ -576,7 +576,8 @@ def _host_type(arr: np.ndarray) -> DType:
 
 
 def execute(a: WorkAssignment, A: np.ndarray, B: np.ndarray, compute: DType = DType.BFloat16,
-            variant: Variant = Variant.Auto, device: int = -1) -> np.ndarray:
+            variant: Variant = Variant.Auto, device: int = -1,
+            out: Optional[np.ndarray] = None) -> np.ndarray:
     """Drop-in of streamk::execute<T> (executor.hpp:130-207): host A (m x k),
     B (k x n) in, new host C (m x n) out, synchronous.
     compute BFloat16/Float16: A/B float32 (rounded on the device), float16 or
@@ -584,7 +585,10 @@ def execute(a: WorkAssignment, A: np.ndarray, B: np.ndarray, compute: DType = DT
     compute Float64 (DMMA): A/B float64, float32 (execute<float>, widened
     exactly, C float32) or int64 (execute<int64_t>, exact, C int64; refused
     unless max|A| max|B| k < 2^53).  The blocking must be the kernel tile of
-    `compute` (kernel_blocking)."""
+    `compute` (kernel_blocking).  `out`: optional C-contiguous m x n array of
+    the C type to write into.  When A, B and out all live in pinned (page-locked)
+    memory and need no conversion, the library overlaps the copies with the
+    kernel (row blocks of A in, finished rows of C out)."""
     p = a.problem
     if A.shape != (p.m, p.k) or B.shape != (p.k, p.n):
         raise ValueError("execute: matrix shapes do not match assignment")
@@ -598,7 +602,12 @@ def execute(a: WorkAssignment, A: np.ndarray, B: np.ndarray, compute: DType = DT
         cdt = {DType.Float64: np.float64, DType.Float32: np.float32, DType.Int64: np.int64}[ht]
     else:
         cdt = np.float32
-    Cm = np.empty((p.m, p.n), cdt)
+    if out is not None:
+        if out.shape != (p.m, p.n) or out.dtype != cdt or not out.flags.c_contiguous:
+            raise ValueError(f"execute: out must be a C-contiguous {p.m}x{p.n} {np.dtype(cdt)} array")
+        Cm = out
+    else:
+        Cm = np.empty((p.m, p.n), cdt)
     if tbl is not None:
         _check(lib().sk_execute_ranges(C.byref(p._c()), C.byref(a.blocking._c()),
                                        tbl.ctypes.data_as(C.c_void_p), tbl.shape[0], int(ht),

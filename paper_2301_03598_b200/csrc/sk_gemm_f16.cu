@@ -192,6 +192,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         // unrelated k offsets by Stream-K units: separate L2 priorities.
         const bool sk_unit = s.strategy == kFixedSplit || s.bal.contains_id(u);
         const uint64_t pol_b = sk_unit ? pol_b_sk : pol_b_dp;
+        if (P.a_ready) wait_flag(P, P.a_ready + tile / s.tiles_n);  // row block of A in HBM
         for (int64_t kb = lb; kb < le; ++kb) {
           ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
           const int32_t k0 = static_cast<int32_t>(kb * BK);
@@ -368,6 +369,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (P.trace && rank == 0) atomicAdd(P.trace + 4 * s.total_tiles + u, 1);
         }
       } else if (!partial) {
+        if (P.c_done) {  // this warp's rows of the tile are in HBM: count them for copy-out
+          if (lane == 0) {
+            ptx::tma_store_wait_all<0>();
+            ptx::fence_proxy_async_global();
+            __threadfence_system();
+            atomicAdd(P.c_done + tile / s.tiles_n, 1);
+          }
+          __syncwarp();
+        }
         if (npeer > 0) {
           ptx::named_bar_sync(1, 32 * EPI_WARPS);
           if (leader)  // every epilogue warp has read the slabs: re-arm the flags
@@ -417,6 +427,7 @@ uint32_t make_idesc_f16(bool bf16, int M, int N) {
 }
 
 size_t f16_slab_bytes() { return sizeof(float) * f16::SLAB_ELEMS; }
+int f16_epilogue_warps() { return f16::EPI_WARPS; }
 
 template <int CG>
 static cudaError_t launch_cg(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,

@@ -97,6 +97,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
                        [&](int64_t, int64_t tile, int64_t lb, int64_t le) {
         const int32_t m0 = static_cast<int32_t>((tile / s.tiles_n) * BM);
         const int32_t n0 = static_cast<int32_t>((tile % s.tiles_n) * BN);
+        if (P.a_ready) wait_flag(P, P.a_ready + tile / s.tiles_n);  // row block of A in HBM
         for (int64_t kb = lb; kb < le; ++kb) {
           ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
           ptx::mbar_expect_tx(&full_bar[stage], STAGE_BYTES);
@@ -240,6 +241,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
             __stcs(dst, acc[i][j][2 * h]);
           }
         }
+    if (P.c_done) {  // the tile is in HBM: count it for copy-out
+      __threadfence_system();
+      ptx::named_bar_sync(1, 128);
+      if (tid == 0) atomicAdd(P.c_done + tile / s.tiles_n, 1);
+    }
     if (ev) {
       if (npeer == 0) ev[kEvWaitEnd] = ev[kEvMacEnd];
       ev[kEvDone] = ptx::globaltimer();

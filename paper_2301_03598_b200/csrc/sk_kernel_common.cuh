@@ -48,6 +48,13 @@ struct KernelParams {
   int64_t watchdog_ns;
   int64_t raster_rows;  // data-parallel tile-row group height (1 = row-major)
   int32_t sk_first;      // TwoTileSkDp phase order: kDpFirst, kSkFirst, kInterleaved
+  // Transfer pipelining (sk_execute with pinned host buffers; NULL otherwise):
+  // a_ready[tile row] turns nonzero once that row block of A has landed (the
+  // producer waits before its first load of the row); c_done[tile row] counts
+  // the row's finished C stores (one per storing epilogue warp) so the copy-out
+  // stream can start on the row before the kernel ends.
+  const int* a_ready;
+  int* c_done;
   int32_t l2_policy[4];  // L2 eviction priority for A loads, B loads (data-parallel
                          // units), C stores, B loads (Stream-K / fixed-split units):
                          // 0 normal, 1 evict_first, 2 evict_last
@@ -59,7 +66,7 @@ struct KernelParams {
 // B panels stay L2-resident; the trailing partial row is visited in order.
 // Only the temporal order changes: unit <-> range <-> tile stays the
 // reference's (decompose.cpp:42-46), so schedule parity is unaffected.
-__device__ __forceinline__ int64_t raster_tile(const Schedule& s, int64_t i, int64_t rows) {
+SK_HD int64_t raster_tile(const Schedule& s, int64_t i, int64_t rows) {
   const int64_t full_rows = s.dp_tiles / s.tiles_n;
   if (rows <= 1 || i >= full_rows * s.tiles_n) return i;
   const int64_t group = rows * s.tiles_n;
@@ -69,7 +76,8 @@ __device__ __forceinline__ int64_t raster_tile(const Schedule& s, int64_t i, int
   return row * s.tiles_n + col;
 }
 
-// The persistent schedule.  Dependencies only run from a tile's owner to
+// The persistent schedule (host-callable too: sk_execute predicts the order in
+// which tile rows of C complete from it).  Dependencies only run from a tile's owner to
 // strictly higher ids inside the balanced (Stream-K) region or inside a
 // fixed-split tile; data-parallel units never wait and are never waited on.
 //   * data-parallel units: physical CTA `cta` of `P` takes slots cta, cta+P, ...
@@ -83,8 +91,9 @@ __device__ __forceinline__ int64_t raster_tile(const Schedule& s, int64_t i, int
 // ids for TwoTileSkDp, below for DpOneTileSk).  Inside a unit, segments run in
 // ascending iteration order (executor.hpp:149-185).  Producer, MMA and epilogue
 // roles all walk this same sequence.
+#pragma nv_exec_check_disable
 template <class F>
-__device__ __forceinline__ void run_unit(const Schedule& s, int64_t u, F& f) {
+SK_HD void run_unit(const Schedule& s, int64_t u, F& f) {
   int64_t b, e;
   s.range(u, &b, &e);
   int64_t it = b;
@@ -101,8 +110,9 @@ __device__ __forceinline__ void run_unit(const Schedule& s, int64_t u, F& f) {
 // Phase orders for TwoTileSkDp (KernelParams::sk_first):
 enum : int { kDpFirst = 0, kSkFirst = 1, kInterleaved = 2 };
 
+#pragma nv_exec_check_disable
 template <class F>
-__device__ __forceinline__ void for_each_segment(const Schedule& s, int64_t cta, int64_t P,
+SK_HD void for_each_segment(const Schedule& s, int64_t cta, int64_t P,
                                                  int64_t raster_rows, F&& f, int order = kDpFirst) {
   auto dp_phase = [&] {
     for (int64_t i = cta; i < s.dp_tiles; i += P) run_unit(s, s.dp_id0 + raster_tile(s, i, raster_rows), f);

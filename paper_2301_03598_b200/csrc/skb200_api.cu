@@ -29,6 +29,7 @@ namespace skb200 {
 // sk_gemm_f16.cu
 uint32_t make_idesc_f16(bool bf16, int M, int N);
 size_t f16_slab_bytes();
+int f16_epilogue_warps();
 cudaError_t launch_f16(int cg, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
                        const KernelParams& p, int grid, cudaStream_t stream);
 // sk_gemm_f64.cu
@@ -361,6 +362,33 @@ sk_status check_desc(const sk_gemm_desc* d, Kernel* kern, Schedule* s) {
 
 }  // namespace
 
+namespace {
+sk_status gemm_impl(const sk_gemm_desc* d, void* ws, size_t ws_bytes, cudaStream_t strm,
+                    const int* a_ready, int* c_done, int64_t raster = 0);
+
+// Raster group height: the group's A panels (rows x BLK_M x k elements) are
+// kept near 32 MB so they stay L2-resident while B streams through; measured
+// best at 8192^3: 16 rows (1-SM), 8 rows (2-SM) (profiles/r01/raster_rows.txt).
+int64_t raster_rows_for(const sk_gemm_desc* d) {
+  const double panel = static_cast<double>(d->blocking.blk_m) * static_cast<double>(d->problem.k) *
+                       static_cast<double>(dtype_size(d->ab_type));
+  int64_t rows = std::max<int64_t>(1, static_cast<int64_t>((32.0 * 1024 * 1024) / panel));
+  if (const char* e = getenv("SKB200_RASTER_ROWS")) rows = std::max(1, atoi(e));
+  return rows;
+}
+
+// TwoTileSkDp phase order: the FP64 kernel runs the SK region first (its fixup
+// epilogues then overlap the DP waves: 33.6 -> 34.3 TFLOP/s at 8192^3); the
+// tcgen05 kernel keeps the DP waves first (SK-first measured 1.5 % slower;
+// interleaving the SK units through the DP waves 4 % slower,
+// profiles/r01/phase_order.txt).
+int phase_order_for(Kernel k) {
+  int order = k == Kernel::F64 ? kSkFirst : kDpFirst;
+  if (const char* e = getenv("SKB200_SK_FIRST")) order = atoi(e);
+  return order;
+}
+}  // namespace
+
 extern "C" {
 
 const char* sk_status_string(sk_status s) {
@@ -563,6 +591,14 @@ extern "C" sk_status sk_timeline_size(const sk_gemm_desc* d, int64_t* records, i
 }
 
 sk_status sk_gemm(const sk_gemm_desc* d, void* ws, size_t ws_bytes, void* stream) {
+  return gemm_impl(d, ws, ws_bytes, static_cast<cudaStream_t>(stream), nullptr, nullptr);
+}
+
+}  // extern "C"
+
+namespace {
+sk_status gemm_impl(const sk_gemm_desc* d, void* ws, size_t ws_bytes, cudaStream_t strm,
+                    const int* a_ready, int* c_done, int64_t raster) {
   Kernel kern;
   Schedule s;
   sk_status st = check_desc(d, &kern, &s);
@@ -591,7 +627,6 @@ sk_status sk_gemm(const sk_gemm_desc* d, void* ws, size_t ws_bytes, void* stream
   if (info.cc_major != 10 || info.cc_minor != 0)
     return fail(SK_EUNSUPPORTED, "device sm_%d%d: this build targets sm_100a only", info.cc_major,
                 info.cc_minor);
-  cudaStream_t strm = static_cast<cudaStream_t>(stream);
   bool upload = false;
   if (ws_prepare(ws, L.flags_off, L.partials_off, L.total, xp ? g_xt.hash : 0, &upload))
     SK_CUDA(cudaMemsetAsync(static_cast<uint8_t*>(ws) + L.flags_off, 0, L.flag_bytes, strm));
@@ -611,6 +646,8 @@ sk_status sk_gemm(const sk_gemm_desc* d, void* ws, size_t ws_bytes, void* stream
   P.flags = reinterpret_cast<int*>(wsb + L.flags_off);
   P.partials = wsb + L.partials_off;
   P.trace = d->trace;
+  P.a_ready = a_ready;
+  P.c_done = c_done;
   P.cta_clocks = reinterpret_cast<long long*>(d->cta_clocks);
   P.events = reinterpret_cast<long long*>(d->events);
   P.seg_stride = d->events ? max_segments_per_unit(s) : 1;
@@ -618,12 +655,7 @@ sk_status sk_gemm(const sk_gemm_desc* d, void* ws, size_t ws_bytes, void* stream
   // Raster group height: the group's A panels (rows x BLK_M x k elements) are
   // kept near 32 MB so they stay L2-resident while B streams through; measured
   // best at 8192^3: 16 rows (1-SM), 8 rows (2-SM) (profiles/r01/raster_rows.txt).
-  {
-    const double panel = static_cast<double>(d->blocking.blk_m) * static_cast<double>(d->problem.k) *
-                         static_cast<double>(dtype_size(d->ab_type));
-    P.raster_rows = std::max<int64_t>(1, static_cast<int64_t>((32.0 * 1024 * 1024) / panel));
-  }
-  if (const char* e = getenv("SKB200_RASTER_ROWS")) P.raster_rows = std::max(1, atoi(e));
+  P.raster_rows = raster > 0 ? raster : raster_rows_for(d);
   // L2 eviction priorities {A loads, B loads, C stores}: 0 normal, 1 first, 2 last.
   // A panels are re-read across a raster group's waves (keep), B panels stream
   // through a wave and C is written once (evict first); measured +4 % at 8192^3
@@ -636,8 +668,7 @@ sk_status sk_gemm(const sk_gemm_desc* d, void* ws, size_t ws_bytes, void* stream
   // TwoTileSkDp phase order: the FP64 kernel runs the SK region first (its fixup
   // epilogues then overlap the DP waves: 33.6 -> 34.3 TFLOP/s at 8192^3); the
   // tcgen05 kernel keeps the DP waves first (SK-first measured 1.5 % slower).
-  P.sk_first = kern == Kernel::F64 ? 1 : 0;
-  if (const char* e = getenv("SKB200_SK_FIRST")) P.sk_first = atoi(e);
+  P.sk_first = phase_order_for(kern);
   if (const char* e = getenv("SKB200_L2_POLICY"))
     sscanf(e, "%d,%d,%d,%d", &P.l2_policy[0], &P.l2_policy[1], &P.l2_policy[2], &P.l2_policy[3]);
   const int64_t units = std::max<int64_t>(s.grid_size, 1);
@@ -693,8 +724,7 @@ sk_status sk_gemm(const sk_gemm_desc* d, void* ws, size_t ws_bytes, void* stream
   }
   return fail(SK_EUNSUPPORTED, "kernel not available");
 }
-
-}  // extern "C"
+}  // namespace
 
 // ---------------------------------------------------------------------------
 // sk_execute: streamk::execute<T> with host buffers (executor.hpp:130-207).
@@ -704,19 +734,28 @@ namespace {
 struct ExecCache {
   int device = -1;
   cudaStream_t stream = nullptr;
-  void* buf[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // A, B, C, ws, staging
-  size_t cap[5] = {0, 0, 0, 0, 0};
+  // transfer pipelining: copy-in and copy-out streams, ordering events
+  cudaStream_t s_in = nullptr, s_out = nullptr;
+  cudaEvent_t ev_in = nullptr, ev_flags = nullptr;
+  void* buf[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};  // A, B, C, ws, staging, row flags
+  size_t cap[6] = {0, 0, 0, 0, 0, 0};
   size_t ws_valid = 0;  // bytes of ws known to be zeroed
   ~ExecCache() { release(); }
   void release() {
     if (device >= 0) cudaSetDevice(device);
-    for (int i = 0; i < 5; ++i) {
+    for (int i = 0; i < 6; ++i) {
       if (buf[i]) cudaFree(buf[i]);
       buf[i] = nullptr;
       cap[i] = 0;
     }
-    if (stream) cudaStreamDestroy(stream);
-    stream = nullptr;
+    for (cudaStream_t* q : {&stream, &s_in, &s_out}) {
+      if (*q) cudaStreamDestroy(*q);
+      *q = nullptr;
+    }
+    for (cudaEvent_t* e : {&ev_in, &ev_flags}) {
+      if (*e) cudaEventDestroy(*e);
+      *e = nullptr;
+    }
     device = -1;
     ws_valid = 0;
   }
@@ -732,6 +771,135 @@ struct ExecCache {
   }
 };
 thread_local ExecCache g_exec;
+
+// cuStreamWaitValue32 (driver API, through the runtime's entry-point query).
+typedef CUresult (*PFN_waitValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+PFN_waitValue32 wait_value32() {
+  static PFN_waitValue32 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return static_cast<PFN_waitValue32>(nullptr);
+    return reinterpret_cast<PFN_waitValue32>(p);
+  }();
+  return fn;
+}
+
+bool is_pinned(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+// Transfer pipelining for sk_execute (pinned host buffers, no conversion): the
+// kernel starts once B is in HBM; A arrives row block by row block on a copy
+// stream (the producer waits on a_ready[row]) and every finished tile row of C
+// leaves on a second copy stream (cuStreamWaitValue32 on c_done[row]) while the
+// kernel still runs, so H2D, compute and D2H overlap.  The schedule is the
+// caller's: only copy order follows it.  Rows are copied in, and waited for,
+// in the order the persistent traversal first needs / last stores them.
+sk_status execute_pipelined(ExecCache& X, sk_gemm_desc& d, size_t ws_bytes, const void* A,
+                            const void* B, void* C, size_t esz, size_t csz, bool zero_c) {
+  Kernel kern;
+  Schedule s;
+  sk_status st = check_desc(&d, &kern, &s);
+  if (st) return st;
+  const int64_t m = d.problem.m, n = d.problem.n, k = d.problem.k, bm = d.blocking.blk_m;
+  const int64_t rows = s.tiles_m;
+  // stores per tile: one per epilogue warp of each CTA of the pair (tcgen05), one (DMMA)
+  const uint32_t incr = kern == Kernel::F64 ? 1u
+                        : static_cast<uint32_t>(kernel_ranks(kern) * f16_epilogue_warps());
+  std::vector<uint32_t> target(static_cast<size_t>(rows), 0);
+  std::vector<int64_t> first(static_cast<size_t>(rows), INT64_MAX), last(static_cast<size_t>(rows), -1);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t P = std::max<int64_t>(1, std::min<int64_t>(std::max<int64_t>(s.grid_size, 1),
+                                                           kern == Kernel::F64 ? 2 * sms : sms / kernel_ranks(kern)));
+  // Row-major data-parallel order: whole rows of C finish early and stream out
+  // while the rest computes (the kernel is a small part of the transfer-bound call).
+  const int64_t raster = 1;
+  const int order = phase_order_for(kern);
+  for (int64_t cta = 0; cta < P; ++cta) {
+    int64_t t = 0;
+    for_each_segment(s, cta, P, raster, [&](int64_t, int64_t tile, int64_t lb, int64_t le) {
+      const size_t r = static_cast<size_t>(tile / s.tiles_n);
+      first[r] = std::min(first[r], t);
+      t += le - lb;
+      if (lb == 0) {
+        last[r] = std::max(last[r], t);
+        target[r] += incr;
+      }
+    }, order);
+  }
+  std::vector<int64_t> in_order(static_cast<size_t>(rows)), out_order;
+  for (int64_t r = 0; r < rows; ++r) in_order[static_cast<size_t>(r)] = r;
+  out_order = in_order;
+  std::stable_sort(in_order.begin(), in_order.end(), [&](int64_t x, int64_t y) {
+    return first[static_cast<size_t>(x)] < first[static_cast<size_t>(y)];
+  });
+  std::stable_sort(out_order.begin(), out_order.end(), [&](int64_t x, int64_t y) {
+    return last[static_cast<size_t>(x)] < last[static_cast<size_t>(y)];
+  });
+
+  st = X.ensure(5, sizeof(int) * static_cast<size_t>(2 * rows));
+  if (st) return st;
+  int* a_ready = static_cast<int*>(X.buf[5]);
+  int* c_done = a_ready + rows;
+  if (!X.s_in) {
+    SK_CUDA(cudaStreamCreateWithFlags(&X.s_in, cudaStreamNonBlocking));
+    SK_CUDA(cudaStreamCreateWithFlags(&X.s_out, cudaStreamNonBlocking));
+    SK_CUDA(cudaEventCreateWithFlags(&X.ev_in, cudaEventDisableTiming));
+    SK_CUDA(cudaEventCreateWithFlags(&X.ev_flags, cudaEventDisableTiming));
+  }
+  cudaStream_t sm = X.stream, si = X.s_in, so = X.s_out;
+  // copy-in: flags down, all of B, then A row blocks (each followed by its flag)
+  SK_CUDA(cudaMemsetAsync(a_ready, 0, sizeof(int) * static_cast<size_t>(2 * rows), si));
+  SK_CUDA(cudaMemcpy2DAsync(X.buf[1], d.ldb * esz, B, n * esz, n * esz, k, cudaMemcpyHostToDevice, si));
+  SK_CUDA(cudaEventRecord(X.ev_in, si));
+  SK_CUDA(cudaStreamWaitEvent(sm, X.ev_in, 0));
+  SK_CUDA(cudaEventRecord(X.ev_flags, sm));  // orders c_done's reset before copy-out waits
+  d.A = X.buf[0];
+  d.B = X.buf[1];
+  d.C = X.buf[2];
+  if (zero_c) SK_CUDA(cudaMemsetAsync(X.buf[2], 0, static_cast<size_t>(m * d.ldc) * csz, sm));
+  st = gemm_impl(&d, X.buf[3], ws_bytes, sm, a_ready, c_done, raster);
+  if (st) return st;
+  const uint8_t* Ah = static_cast<const uint8_t*>(A);
+  uint8_t* Ad = static_cast<uint8_t*>(X.buf[0]);
+  for (int64_t r : in_order) {
+    const int64_t r0 = r * bm, nr = std::min(bm, m - r0);
+    SK_CUDA(cudaMemcpy2DAsync(Ad + static_cast<size_t>(r0 * d.lda) * esz, d.lda * esz,
+                              Ah + static_cast<size_t>(r0 * k) * esz, k * esz, k * esz, nr,
+                              cudaMemcpyHostToDevice, si));
+    SK_CUDA(cudaMemsetAsync(a_ready + r, 1, 1, si));
+  }
+  // copy-out: each tile row once all of its stores have landed
+  SK_CUDA(cudaStreamWaitEvent(so, X.ev_flags, 0));
+  uint8_t* Ch = static_cast<uint8_t*>(C);
+  const uint8_t* Cd = static_cast<const uint8_t*>(X.buf[2]);
+  PFN_waitValue32 wv = wait_value32();
+  for (int64_t r : out_order) {
+    const int64_t r0 = r * bm, nr = std::min(bm, m - r0);
+    if (target[static_cast<size_t>(r)]) {
+      const CUresult cr = wv(reinterpret_cast<CUstream>(so), reinterpret_cast<CUdeviceptr>(c_done + r),
+                             target[static_cast<size_t>(r)], CU_STREAM_WAIT_VALUE_GEQ);
+      if (cr != CUDA_SUCCESS) return fail(SK_ECUDA, "cuStreamWaitValue32 failed (%d)", int(cr));
+    } else {
+      SK_CUDA(cudaStreamWaitEvent(so, X.ev_flags, 0));
+    }
+    SK_CUDA(cudaMemcpy2DAsync(Ch + static_cast<size_t>(r0 * n) * csz, n * csz,
+                              Cd + static_cast<size_t>(r0 * d.ldc) * csz, d.ldc * csz, n * csz, nr,
+                              cudaMemcpyDeviceToHost, so));
+  }
+  SK_CUDA(cudaStreamSynchronize(si));
+  SK_CUDA(cudaStreamSynchronize(so));
+  return sk_workspace_check(X.buf[3], sm);
+}
 
 int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
@@ -813,6 +981,14 @@ sk_status execute_impl(const sk_problem* p, const sk_blocking* b, sk_strategy st
     st = sk_workspace_init(X.buf[3], X.cap[3], s);
     if (st) return st;
     X.ws_valid = X.cap[3];
+  }
+  // Overlapped transfers: pinned host buffers, no element conversion, > 1 tile row.
+  {
+    const bool same = is16 ? host_type == compute_type : host_type == SK_FLOAT64;
+    const char* e = getenv("SKB200_PIPELINE");
+    if (same && !(e && atoi(e) == 0) && m > b->blk_m && wait_value32() && is_pinned(A) &&
+        is_pinned(B) && is_pinned(C))
+      return execute_pipelined(X, d, ws_bytes, A, B, C, esz, csz, zero_c);
   }
   if (host_type == SK_FLOAT32 && is16) {
     // H2D fp32, round-to-nearest-even into the pitched 16-bit operand buffers.
