@@ -786,6 +786,27 @@ PFN_waitValue32 wait_value32() {
   return fn;
 }
 
+// Pitched copy that degenerates to one linear copy when both pitches equal the width.
+cudaError_t copy_rows(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width,
+                      int64_t rows, cudaMemcpyKind kind, cudaStream_t q) {
+  if (dpitch == width && spitch == width)
+    return cudaMemcpyAsync(dst, src, width * static_cast<size_t>(rows), kind, q);
+  return cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, static_cast<size_t>(rows), kind, q);
+}
+
+typedef CUresult (*PFN_writeValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+PFN_writeValue32 write_value32() {
+  static PFN_writeValue32 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return static_cast<PFN_writeValue32>(nullptr);
+    return reinterpret_cast<PFN_writeValue32>(p);
+  }();
+  return fn;
+}
+
 bool is_pinned(const void* p) {
   cudaPointerAttributes a;
   if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
@@ -859,7 +880,7 @@ sk_status execute_pipelined(ExecCache& X, sk_gemm_desc& d, size_t ws_bytes, cons
   cudaStream_t sm = X.stream, si = X.s_in, so = X.s_out;
   // copy-in: flags down, all of B, then A row blocks (each followed by its flag)
   SK_CUDA(cudaMemsetAsync(a_ready, 0, sizeof(int) * static_cast<size_t>(2 * rows), si));
-  SK_CUDA(cudaMemcpy2DAsync(X.buf[1], d.ldb * esz, B, n * esz, n * esz, k, cudaMemcpyHostToDevice, si));
+  SK_CUDA(copy_rows(X.buf[1], d.ldb * esz, B, n * esz, n * esz, k, cudaMemcpyHostToDevice, si));
   SK_CUDA(cudaEventRecord(X.ev_in, si));
   SK_CUDA(cudaStreamWaitEvent(sm, X.ev_in, 0));
   SK_CUDA(cudaEventRecord(X.ev_flags, sm));  // orders c_done's reset before copy-out waits
@@ -871,30 +892,51 @@ sk_status execute_pipelined(ExecCache& X, sk_gemm_desc& d, size_t ws_bytes, cons
   if (st) return st;
   const uint8_t* Ah = static_cast<const uint8_t*>(A);
   uint8_t* Ad = static_cast<uint8_t*>(X.buf[0]);
-  for (int64_t r : in_order) {
-    const int64_t r0 = r * bm, nr = std::min(bm, m - r0);
-    SK_CUDA(cudaMemcpy2DAsync(Ad + static_cast<size_t>(r0 * d.lda) * esz, d.lda * esz,
-                              Ah + static_cast<size_t>(r0 * k) * esz, k * esz, k * esz, nr,
-                              cudaMemcpyHostToDevice, si));
-    SK_CUDA(cudaMemsetAsync(a_ready + r, 1, 1, si));
+  // Consecutive row blocks travel as one copy of up to ~16 MB (per-copy gaps
+  // cost more than the later first row, profiles/r01/pipeline.txt).
+  const int64_t max_rows = std::max<int64_t>(1, (int64_t(16) << 20) / std::max<int64_t>(1, bm * k * static_cast<int64_t>(esz)));
+  for (size_t i = 0; i < in_order.size();) {
+    size_t j = i + 1;
+    while (j < in_order.size() && in_order[j] == in_order[j - 1] + 1 &&
+           static_cast<int64_t>(j - i) < max_rows)
+      ++j;
+    const int64_t r0 = in_order[i] * bm, nr = std::min(in_order[j - 1] * bm + bm, m) - r0;
+    SK_CUDA(copy_rows(Ad + static_cast<size_t>(r0 * d.lda) * esz, d.lda * esz,
+                      Ah + static_cast<size_t>(r0 * k) * esz, k * esz, k * esz, nr,
+                      cudaMemcpyHostToDevice, si));
+    // a stream memory op, not a memset kernel: nothing may need an SM the
+    // persistent GEMM is holding
+    for (size_t q = i; q < j; ++q) {
+      const CUresult cr = write_value32()(reinterpret_cast<CUstream>(si),
+                                          reinterpret_cast<CUdeviceptr>(a_ready + in_order[q]), 1,
+                                          CU_STREAM_WRITE_VALUE_DEFAULT);
+      if (cr != CUDA_SUCCESS) return fail(SK_ECUDA, "cuStreamWriteValue32 failed (%d)", int(cr));
+    }
+    i = j;
   }
   // copy-out: each tile row once all of its stores have landed
   SK_CUDA(cudaStreamWaitEvent(so, X.ev_flags, 0));
   uint8_t* Ch = static_cast<uint8_t*>(C);
   const uint8_t* Cd = static_cast<const uint8_t*>(X.buf[2]);
   PFN_waitValue32 wv = wait_value32();
-  for (int64_t r : out_order) {
-    const int64_t r0 = r * bm, nr = std::min(bm, m - r0);
-    if (target[static_cast<size_t>(r)]) {
+  const int64_t max_out = std::max<int64_t>(1, (int64_t(16) << 20) / std::max<int64_t>(1, bm * n * static_cast<int64_t>(csz)));
+  for (size_t i = 0; i < out_order.size();) {
+    size_t j = i + 1;
+    while (j < out_order.size() && out_order[j] == out_order[j - 1] + 1 &&
+           static_cast<int64_t>(j - i) < max_out)
+      ++j;
+    for (size_t q = i; q < j; ++q) {
+      const int64_t r = out_order[q];
+      if (!target[static_cast<size_t>(r)]) continue;  // nothing stores it (explicit tables)
       const CUresult cr = wv(reinterpret_cast<CUstream>(so), reinterpret_cast<CUdeviceptr>(c_done + r),
                              target[static_cast<size_t>(r)], CU_STREAM_WAIT_VALUE_GEQ);
       if (cr != CUDA_SUCCESS) return fail(SK_ECUDA, "cuStreamWaitValue32 failed (%d)", int(cr));
-    } else {
-      SK_CUDA(cudaStreamWaitEvent(so, X.ev_flags, 0));
     }
-    SK_CUDA(cudaMemcpy2DAsync(Ch + static_cast<size_t>(r0 * n) * csz, n * csz,
-                              Cd + static_cast<size_t>(r0 * d.ldc) * csz, d.ldc * csz, n * csz, nr,
-                              cudaMemcpyDeviceToHost, so));
+    const int64_t r0 = out_order[i] * bm, nr = std::min(out_order[j - 1] * bm + bm, m) - r0;
+    SK_CUDA(copy_rows(Ch + static_cast<size_t>(r0 * n) * csz, n * csz,
+                      Cd + static_cast<size_t>(r0 * d.ldc) * csz, d.ldc * csz, n * csz, nr,
+                      cudaMemcpyDeviceToHost, so));
+    i = j;
   }
   SK_CUDA(cudaStreamSynchronize(si));
   SK_CUDA(cudaStreamSynchronize(so));
@@ -986,7 +1028,7 @@ sk_status execute_impl(const sk_problem* p, const sk_blocking* b, sk_strategy st
   {
     const bool same = is16 ? host_type == compute_type : host_type == SK_FLOAT64;
     const char* e = getenv("SKB200_PIPELINE");
-    if (same && !(e && atoi(e) == 0) && m > b->blk_m && wait_value32() && is_pinned(A) &&
+    if (same && !(e && atoi(e) == 0) && m > b->blk_m && wait_value32() && write_value32() && is_pinned(A) &&
         is_pinned(B) && is_pinned(C))
       return execute_pipelined(X, d, ws_bytes, A, B, C, esz, csz, zero_c);
   }
