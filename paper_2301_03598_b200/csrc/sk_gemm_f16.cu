@@ -193,7 +193,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const bool sk_unit = s.strategy == kFixedSplit || s.bal.contains_id(u);
         const uint64_t pol_b = sk_unit ? pol_b_sk : pol_b_dp;
         if (P.a_ready) wait_flag(P, P.a_ready + tile / s.tiles_n);  // row block of A in HBM
-        for (int64_t kb = lb; kb < le; ++kb) {
+        // k order of a balanced unit's segments (P.k_align): see k_block_of.
+        int64_t rot = -1;
+        if (P.k_align && sk_unit && s.strategy != kFixedSplit) {
+          int64_t b, e;
+          s.range(u, &b, &e);
+          rot = k_rotation(s, b, e, tile, lb, le);
+        }
+        for (int64_t i = lb; i < le; ++i) {
+          const int64_t kb = rot < 0 ? i : k_block_of(s.ipt, lb, le, rot, i - lb);
           ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
           const int32_t k0 = static_cast<int32_t>(kb * BK);
           uint8_t* a_dst = sA + stage * K::A_STAGE;

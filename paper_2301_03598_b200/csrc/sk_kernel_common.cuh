@@ -55,6 +55,7 @@ struct KernelParams {
   // stream can start on the row before the kernel ends.
   const int* a_ready;
   int* c_done;
+  int32_t k_align;  // balanced units: aligned k order (k_block_of), 0 = ascending
   int32_t l2_policy[4];  // L2 eviction priority for A loads, B loads (data-parallel
                          // units), C stores, B loads (Stream-K / fixed-split units):
                          // 0 normal, 1 evict_first, 2 evict_last
@@ -147,6 +148,30 @@ SK_HD void for_each_segment(const Schedule& s, int64_t cta, int64_t P,
     desc_phase(s.bal.first_id, s.bal.first_id + s.bal.count);
     dp_phase();
   }
+}
+
+// k-block order inside a balanced unit's tile segment (the set of k-blocks is
+// the reference's; only the order in which they are multiplied changes, which
+// keeps integer-valued results exact and every result deterministic).  All
+// balanced units start together and run at the same rate, so a unit-local clock
+// tau (iterations since the unit began) is a common clock.  Walking a segment
+// that starts mid-tile, [lb, ipt), DOWNWARD reads k-block ipt - 1 - tau at time
+// tau in every unit, and walking the unit's last segment, [0, le), downward
+// reads (L - 1 - tau) mod ipt (L = unit length); a full middle tile is rotated
+// onto that same phase.  Readers of one B column panel then meet on (at most
+// two phases of) the same k-block at the same time instead of at unrelated
+// offsets, so the panel is fetched from HBM once per phase, not once per tile.
+SK_HD int64_t k_rotation(const Schedule& s, int64_t b, int64_t e, int64_t tile, int64_t lb,
+                         int64_t le) {
+  if (le - lb < s.ipt) return 0;  // partial or last segment: plain descending
+  const int64_t t0 = tile * s.ipt - b;  // unit-local time this full segment starts
+  const int64_t r = (e - b - 1 - t0) % s.ipt;
+  return r < 0 ? r + s.ipt : r;
+}
+SK_HD int64_t k_block_of(int64_t ipt, int64_t lb, int64_t le, int64_t rot, int64_t i) {
+  if (le - lb < ipt) return le - 1 - i;
+  const int64_t k = rot - i;
+  return k < 0 ? k + ipt : k;
 }
 
 // Per-CTA clock stamps (sk_gemm_desc.cta_clocks): the effective SM clock of a

@@ -669,6 +669,11 @@ sk_status gemm_impl(const sk_gemm_desc* d, void* ws, size_t ws_bytes, cudaStream
   // epilogues then overlap the DP waves: 33.6 -> 34.3 TFLOP/s at 8192^3); the
   // tcgen05 kernel keeps the DP waves first (SK-first measured 1.5 % slower).
   P.sk_first = phase_order_for(kern);
+  // Balanced units walk their k-blocks against a common clock (k_block_of): B
+  // panels are shared in time across the SK region; 8192^3 hybrid 1458 -> 1482
+  // TFLOP/s, config-3 geomean 1.287 -> 1.325 (profiles/r01/k_align.txt).
+  P.k_align = kern == Kernel::F64 ? 0 : 1;
+  if (const char* e = getenv("SKB200_K_ALIGN")) P.k_align = atoi(e);
   if (const char* e = getenv("SKB200_L2_POLICY"))
     sscanf(e, "%d,%d,%d,%d", &P.l2_policy[0], &P.l2_policy[1], &P.l2_policy[2], &P.l2_policy[3]);
   const int64_t units = std::max<int64_t>(s.grid_size, 1);
