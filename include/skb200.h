@@ -216,6 +216,12 @@ sk_status sk_trace_size(const sk_gemm_desc* desc, int64_t* ints);
 /* Records of the optional device timeline: grid_size * seg_stride (record of
  * unit u's i-th tile segment at u * seg_stride + i; unused records stay zero). */
 sk_status sk_timeline_size(const sk_gemm_desc* desc, int64_t* records, int64_t* seg_stride);
+/* Two-die topology of a device as the die-aware schedule sees it (probed once
+ * per device, synchronising): *ok = 1 and die_of_sm[0..*sms) in {0, 1} when
+ * the device shows a clean two-die split with TPC-aligned 2-CTA clusters, else
+ * *ok = 0.  die_of_sm may be NULL; at most max_sms entries are written. */
+sk_status sk_device_topology(int device, int32_t* die_of_sm, int32_t max_sms, int32_t* sms,
+                             int32_t* ok);
 /* Stream-ordered, asynchronous.  Does not synchronise. */
 sk_status sk_gemm(const sk_gemm_desc* desc, void* workspace, size_t workspace_bytes,
                   void* stream);

@@ -32,7 +32,8 @@ from typing import List, Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libskb200.so")
+# SKB200_LIB: load an alternative build of the library (kernel experiments)
+LIB_PATH = os.environ.get("SKB200_LIB") or os.path.join(_HERE, "_lib", "libskb200.so")
 
 __all__ = [
     "DType", "Strategy", "HybridVariant", "Variant", "GemmProblem", "BlockingFactors", "TileGrid",
@@ -110,6 +111,7 @@ _SIGS = {
     "sk_trace_size": (C.c_int, [_P(sk_gemm_desc), _P(C.c_int64)]),
     "sk_timeline_size": (C.c_int, [_P(sk_gemm_desc), _P(C.c_int64), _P(C.c_int64)]),
     "sk_gemm": (C.c_int, [_P(sk_gemm_desc), C.c_void_p, C.c_size_t, C.c_void_p]),
+    "sk_device_topology": (C.c_int, [C.c_int, C.c_void_p, C.c_int32, _P(C.c_int32), _P(C.c_int32)]),
     "sk_execute": (C.c_int, [_P(sk_problem), _P(sk_blocking), C.c_int, C.c_int64, C.c_int, C.c_int,
                              C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32]),
     "sk_execute_ranges": (C.c_int, [_P(sk_problem), _P(sk_blocking), C.c_void_p, C.c_int64, C.c_int,
@@ -559,6 +561,16 @@ def kernel_blocking(ab_type: DType = DType.BFloat16, variant: Variant = Variant.
     out = sk_blocking()
     _check(lib().sk_kernel_blocking(int(ab_type), int(variant), C.byref(out)), "kernel_blocking")
     return BlockingFactors(out.blk_m, out.blk_n, out.blk_k)
+
+
+def device_topology(device: int = 0) -> Optional[np.ndarray]:
+    """Die of each SM (0/1) as probed by the library for the die-aware
+    data-parallel phase, or None when the device shows no clean two-die split."""
+    die = np.zeros(256, np.int32)
+    sms, ok = C.c_int32(0), C.c_int32(0)
+    _check(lib().sk_device_topology(device, die.ctypes.data_as(C.c_void_p), 256, C.byref(sms),
+                                    C.byref(ok)), "device_topology")
+    return die[:sms.value].copy() if ok.value else None
 
 
 def _host_type(arr: np.ndarray) -> DType:

@@ -121,6 +121,9 @@ __device__ __forceinline__ void tma_load_2d_to_leader(void* dst, const CUtensorM
       "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(bar_cluster_addr), "l"(policy)
       : "memory");
 }
+__device__ __forceinline__ void st_shared_cluster(uint32_t addr, int v) {
+  asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
 __device__ __forceinline__ void mbar_arrive_remote(uint32_t bar_cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster_addr)
                : "memory");
@@ -143,6 +146,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* tfull_bar = empty_bar + K::STAGES;
   uint64_t* tempty_bar = tfull_bar + 2;
   uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  int* lane_code_smem = reinterpret_cast<int*>(tmem_base_smem + 1);
 
   const uint32_t warp = threadIdx.x / 32;
   const uint32_t lane = threadIdx.x % 32;
@@ -164,6 +168,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       ptx::mbar_init(&tempty_bar[i], EPI_WARPS * CG);
     }
     ptx::fence_barrier_init();
+    // Die-aware DP lane (die_lane): keyed by the leader CTA's SM, shared with the peer.
+    if (P.die_aware && leader_cta) {
+      const int code = P.die_tab[ptx::smid()];
+      *lane_code_smem = code;
+      if constexpr (CG == 2) st_shared_cluster(mapa(lane_code_smem, 1), code);
+    }
   }
   if (warp == 1) ptx::tmem_alloc<CG>(tmem_base_smem, TMEM_COLS);
   ptx::tc_fence_before();
@@ -171,6 +181,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if constexpr (CG == 2) cluster_sync();  // peer barriers initialised before any remote use
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_base_smem;
+  DpLane dp_lane = default_lane(s, cta, P.num_ctas);
+  if (P.die_aware) {
+    const int code = *lane_code_smem;
+    if (code >= 0) dp_lane = die_lane(s, P.die_n, code);
+    else if (threadIdx.x == 0) atomicOr(P.err, kErrTopology);  // host validated: unreachable
+  }
   // Programmatic dependent launch: the prologue above overlaps the previous
   // kernel's tail; nothing below touches global memory before it completes.
   ptx::grid_dependency_wait();
@@ -184,7 +200,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const uint64_t pol_b_dp = ptx::make_policy(P.l2_policy[1]);
       const uint64_t pol_b_sk = ptx::make_policy(P.l2_policy[3]);
       uint32_t stage = 0, phase = 0;
-      for_each_segment(s, cta, P.num_ctas, P.raster_rows,
+      for_each_segment(s, cta, P.num_ctas, dp_lane, P.raster_rows,
                        [&](int64_t u, int64_t tile, int64_t lb, int64_t le) {
         const int32_t m0 = static_cast<int32_t>((tile / s.tiles_n) * (ROWS * CG) + rank * ROWS);
         const int32_t n0 = static_cast<int32_t>((tile % s.tiles_n) * BN + rank * K::B_COLS);
@@ -233,7 +249,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // ===================== tcgen05.mma issuer =====================
     if (lane == 0 && leader_cta) {
       uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
-      for_each_segment(s, cta, P.num_ctas, P.raster_rows,
+      for_each_segment(s, cta, P.num_ctas, dp_lane, P.raster_rows,
                        [&](int64_t u, int64_t tile, int64_t lb, int64_t le) {
         ptx::mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         ptx::tc_fence_after();
@@ -280,7 +296,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     uint32_t acc = 0, acc_phase = 0, nstores = 0;
     // flag / slab index of a (unit, rank): each CTA of a pair runs its own protocol
     auto fidx = [&](int64_t u) { return s.slab_of(u) * CG + rank; };
-    for_each_segment(s, cta, P.num_ctas, P.raster_rows,
+    for_each_segment(s, cta, P.num_ctas, dp_lane, P.raster_rows,
                      [&](int64_t u, int64_t tile, int64_t lb, int64_t le) {
       ptx::mbar_wait(&tfull_bar[acc], acc_phase);
       ptx::tc_fence_after();

@@ -29,10 +29,12 @@ struct WorkspaceLayout {
 };
 
 // Error word bits.
-enum : int { kErrDoubleSignal = 1, kErrWatchdog = 1 << 16 };
+enum : int { kErrDoubleSignal = 1, kErrWatchdog = 1 << 16, kErrTopology = 1 << 17 };
 
 // Trace layout (ints): per tile {owner, last_peer, storing_unit, segments_folded},
 // then per unit {partials_emitted}.
+constexpr int kMaxSms = 192;
+
 struct KernelParams {
   Schedule s;
   int64_t num_ctas;  // persistent CTAs (pairs for the 2-SM kernel)
@@ -59,7 +61,34 @@ struct KernelParams {
   int32_t l2_policy[4];  // L2 eviction priority for A loads, B loads (data-parallel
                          // units), C stores, B loads (Stream-K / fixed-split units):
                          // 0 normal, 1 evict_first, 2 evict_last
+  // Die-aware data-parallel phase (see dp_lane): B200 is two dies, each with
+  // half of the SMs and its own L2; die_tab[smid] = die << 8 | rank of the
+  // persistent CTA (pair) among those of its die, -1 unknown.  die_n = CTAs
+  // (pairs) per die.  Only set for a full persistent grid on a probed device.
+  int32_t die_aware;
+  int32_t die_n[2];
+  int16_t die_tab[kMaxSms];
 };
+
+// The data-parallel slots [first, end) with stride `step` that one persistent
+// CTA walks (in the rasterised order).  Default: slot cta, cta + P, ...
+struct DpLane {
+  int64_t first, step, end;
+};
+SK_HD DpLane default_lane(const Schedule& s, int64_t cta, int64_t P) {
+  return DpLane{cta, P, s.dp_tiles};
+}
+// Die-aware lane: the rasterised DP order is cut in two contiguous ranges,
+// sized by the dies' CTA counts; the CTAs of die d stride through range d only.
+// Each die's L2 then holds its own A panels and one compact wave of B panels
+// instead of both dies caching (and missing on) the union: measured on 8192^3
+// (profiles/r01/die_aware.txt).  `code` = die << 8 | rank from die_tab.
+SK_HD DpLane die_lane(const Schedule& s, const int32_t* die_n, int code) {
+  const int d = (code >> 8) & 1, r = code & 0xff;
+  const int64_t P = die_n[0] + die_n[1];
+  const int64_t t0 = (s.dp_tiles * die_n[0] + P / 2) / P;
+  return d == 0 ? DpLane{r, die_n[0], t0} : DpLane{t0 + r, die_n[1], s.dp_tiles};
+}
 
 // Data-parallel slot i -> tile, a bijection on [0, dp_tiles): whole tile rows
 // are visited in groups of `rows` rows, column-major inside a group, so one
@@ -113,10 +142,11 @@ enum : int { kDpFirst = 0, kSkFirst = 1, kInterleaved = 2 };
 
 #pragma nv_exec_check_disable
 template <class F>
-SK_HD void for_each_segment(const Schedule& s, int64_t cta, int64_t P,
-                                                 int64_t raster_rows, F&& f, int order = kDpFirst) {
+SK_HD void for_each_segment(const Schedule& s, int64_t cta, int64_t P, const DpLane& lane,
+                            int64_t raster_rows, F&& f, int order = kDpFirst) {
   auto dp_phase = [&] {
-    for (int64_t i = cta; i < s.dp_tiles; i += P) run_unit(s, s.dp_id0 + raster_tile(s, i, raster_rows), f);
+    for (int64_t i = lane.first; i < lane.end; i += lane.step)
+      run_unit(s, s.dp_id0 + raster_tile(s, i, raster_rows), f);
   };
   auto desc_phase = [&](int64_t lo, int64_t hi) {
     for (int64_t u = hi - 1 - cta; u >= lo; u -= P) run_unit(s, u, f);
@@ -148,6 +178,13 @@ SK_HD void for_each_segment(const Schedule& s, int64_t cta, int64_t P,
     desc_phase(s.bal.first_id, s.bal.first_id + s.bal.count);
     dp_phase();
   }
+}
+
+#pragma nv_exec_check_disable
+template <class F>
+SK_HD void for_each_segment(const Schedule& s, int64_t cta, int64_t P, int64_t raster_rows, F&& f,
+                            int order = kDpFirst) {
+  for_each_segment(s, cta, P, default_lane(s, cta, P), raster_rows, static_cast<F&&>(f), order);
 }
 
 // k-block order inside a balanced unit's tile segment (the set of k-blocks is

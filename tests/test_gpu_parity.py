@@ -430,3 +430,42 @@ def test_execute_drop_in_all_reference_types(sk, port, ref):
     big = np.full((8, 8), 2 ** 40, np.int64)
     with pytest.raises(sk.UnsupportedError):
         sk.execute(sk.data_parallel(sk.GemmProblem(8, 8, 8), blk), big, big, compute=sk.DType.Float64)
+
+
+# ---------------------------------------------------------------- die-aware lanes
+def test_device_topology_two_dies(sk, torch_cuda):
+    """sk_device_topology: a B200 shows two dies, TPC pairs never straddle them."""
+    die = sk.device_topology(0)
+    sms = torch_cuda.cuda.get_device_properties(0).multi_processor_count
+    assert die is not None and len(die) == sms
+    assert set(die.tolist()) == {0, 1}
+    assert all(die[2 * t] == die[2 * t + 1] for t in range(sms // 2))
+
+
+@pytest.mark.parametrize("var", VARIANTS)
+def test_die_aware_lanes_bit_exact(sk, torch_cuda, monkeypatch, var):
+    """SKB200_DIE_AWARE=1 only re-maps data-parallel tiles to persistent CTAs:
+    the full-grid schedules give the same C (bit-identical) with and without it,
+    and the integer-valued 2048^3 result stays exact (row checksums)."""
+    torch = torch_cuda
+    m = n = k = 2048
+    V = variant(sk, var)
+    blk = sk.kernel_blocking(sk.DType.BFloat16, V)
+    p = 148 if V == sk.Variant.OneSM else 74
+    g = torch.Generator(device="cuda").manual_seed(3)
+    A = torch.randint(-2, 2, (m, k), device="cuda", generator=g).to(torch.bfloat16)
+    B = torch.randint(-2, 2, (k, n), device="cuda", generator=g).to(torch.bfloat16)
+    rows = (A.double() @ (B.double() @ torch.ones(n, 1, device="cuda", dtype=torch.float64))).squeeze(1)
+    prob = sk.GemmProblem(m, n, k)
+    for a in (sk.data_parallel(prob, blk), sk.hybrid(prob, blk, p, sk.HybridVariant.TwoTileSkDp),
+              sk.hybrid(prob, blk, p, sk.HybridVariant.DpOneTileSk)):
+        out = []
+        for flag in ("0", "1"):
+            monkeypatch.setenv("SKB200_DIE_AWARE", flag)
+            C = torch.full((m, n), float("nan"), device="cuda")
+            gemm = sk.Gemm(a, variant=V)
+            gemm.run(A, B, C)
+            gemm.check()
+            out.append(C)
+        assert torch.equal(out[0], out[1])
+        assert torch.equal(out[1].double().sum(1), rows)
