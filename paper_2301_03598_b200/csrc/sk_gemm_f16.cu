@@ -296,6 +296,109 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     uint32_t acc = 0, acc_phase = 0, nstores = 0;
     // flag / slab index of a (unit, rank): each CTA of a pair runs its own protocol
     auto fidx = [&](int64_t u) { return s.slab_of(u) * CG + rank; };
+    const int64_t own_base = s.num_slabs * CG;  // cooperative: owners' published accumulators
+    const int64_t done_base = 2 * s.num_slabs * CG;
+    const int64_t bal_tile0 = s.bal.begin / s.ipt;
+    auto slab = [&](int64_t idx) { return partials + idx * static_cast<int64_t>(SLAB_ELEMS); };
+    const int c_lo = static_cast<int>((warp - 2) / 4) * (EPI_COLS / 32);
+    // One 32x32 fp32 box of C (this warp's rows, 32 columns at n0 + 32 * c): stage
+    // through a ring of EPI_BUFS swizzled smem boxes (16-B chunk j of row r at
+    // j ^ (r % 8)); EPI_BUFS - 1 TMA stores stay in flight while the next is written.
+    auto store_box = [&](const float* v32, int32_t n0, int32_t m0, int c) {
+      float* buf = stage_buf + (nstores % EPI_BUFS) * (EPI_BUF_BYTES / 4);
+      if (nstores >= EPI_BUFS) {
+        if (lane == 0) ptx::tma_store_wait_read<EPI_BUFS - 1>();
+        __syncwarp();
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int jj = j ^ static_cast<int>(lane & 7);
+        *reinterpret_cast<float4*>(buf + lane * 32 + jj * 4) =
+            make_float4(v32[4 * j], v32[4 * j + 1], v32[4 * j + 2], v32[4 * j + 3]);
+      }
+      ptx::fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        ptx::tma_store_2d_hint(&tmC, buf, n0 + c * 32, m0 + static_cast<int32_t>(q * 32), pol_c);
+        ptx::tma_store_commit();
+      }
+      ++nstores;
+    };
+    // Cooperative fold of one shared tile by contributor u: wait for every
+    // contributor's slab, fold the 32-column chunks c = idx, idx + ncon, ...
+    // (owner's accumulator, then peers ascending: executor.hpp:165-172), store
+    // them, and let the last contributor to finish re-arm the tile's flags.
+    auto coop_fold = [&](int64_t u, int64_t tile) {
+      int64_t owner, last;
+      s.peers(tile, &owner, &last);
+      const int ncon = static_cast<int>(last - owner + 1);
+      const int idx = static_cast<int>(u - owner);
+      const int32_t m0 = static_cast<int32_t>((tile / s.tiles_n) * (ROWS * CG) + rank * ROWS);
+      const int32_t n0 = static_cast<int32_t>((tile % s.tiles_n) * BN);
+      if (idx < EPI_COLS / 32) {  // else: no chunk to fold (more contributors than chunks)
+        if (lane == 0) {
+          wait_flag(P, P.flags + own_base + fidx(owner));
+          for (int64_t pu = owner + 1; pu <= last; ++pu) wait_flag(P, P.flags + fidx(pu));
+        }
+        __syncwarp();
+        const float* os = slab(own_base + fidx(owner));
+#pragma unroll 1
+        for (int c = c_lo + idx; c < c_lo + EPI_COLS / 32; c += ncon) {
+          float4 a[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) a[j] = ptx::ld_cg_f4(slab_ptr(const_cast<float*>(os), c, j, row));
+          int64_t pu = owner + 1;
+#pragma unroll 1
+          for (; pu + 1 <= last; pu += 2) {  // two peer slabs in flight, folded in id order
+            float* p0 = slab(fidx(pu));
+            float* p1 = slab(fidx(pu + 1));
+            float4 w0[8], w1[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              w0[j] = ptx::ld_cg_f4(slab_ptr(p0, c, j, row));
+              w1[j] = ptx::ld_cg_f4(slab_ptr(p1, c, j, row));
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              a[j].x += w0[j].x; a[j].y += w0[j].y; a[j].z += w0[j].z; a[j].w += w0[j].w;
+              a[j].x += w1[j].x; a[j].y += w1[j].y; a[j].z += w1[j].z; a[j].w += w1[j].w;
+            }
+          }
+          if (pu <= last) {
+            float* p0 = slab(fidx(pu));
+            float4 w0[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) w0[j] = ptx::ld_cg_f4(slab_ptr(p0, c, j, row));
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              a[j].x += w0[j].x; a[j].y += w0[j].y; a[j].z += w0[j].z; a[j].w += w0[j].w;
+            }
+          }
+          // Every lane has consumed the chunk: its slab lines are dead, drop them
+          // from L2 without a write-back (lane l: line l of the warp's 4 KB).
+          __syncwarp();
+          ptx::discard_l2(reinterpret_cast<const char*>(slab_ptr(const_cast<float*>(os), c, lane / 4, q * 32)) +
+                          (lane % 4) * 128);
+          for (int64_t pd = owner + 1; pd <= last; ++pd)
+            ptx::discard_l2(reinterpret_cast<const char*>(slab_ptr(slab(fidx(pd)), c, lane / 4, q * 32)) +
+                            (lane % 4) * 128);
+          store_box(reinterpret_cast<const float*>(a), n0, m0, c);
+        }
+      }
+      // every epilogue warp of this CTA has read its slabs: count the contributor
+      ptx::named_bar_sync(1, 32 * EPI_WARPS);
+      if (leader) {
+        int* done = P.flags + done_base + (tile - bal_tile0) * CG + rank;
+        __threadfence();
+        if (atomicAdd(done, 1) == ncon - 1) {  // the last reader re-arms the tile
+          ptx::st_relaxed(P.flags + own_base + fidx(owner), 0);
+          for (int64_t pu = owner + 1; pu <= last; ++pu) ptx::st_relaxed(P.flags + fidx(pu), 0);
+          ptx::st_relaxed(done, 0);
+        }
+      }
+    };
+    int64_t pend0 = 0, pend1 = 0;  // this unit's published shared tiles (at most two)
+    int npend = 0;
     for_each_segment(s, cta, P.num_ctas, dp_lane, P.raster_rows,
                      [&](int64_t u, int64_t tile, int64_t lb, int64_t le) {
       ptx::mbar_wait(&tfull_bar[acc], acc_phase);
@@ -308,21 +411,26 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const bool partial = lb != 0;  // not the tile starter (executor.hpp:160)
       const bool orphan = partial && s.orphan(tile);  // explicit table: nobody folds it
       const int npeer = (!partial && (le < s.ipt || s.strategy == kExplicit)) ? s.npeers(tile, u) : 0;
-      if (npeer > 0) {
+      // Cooperative schedule: the owner of a shared tile publishes its
+      // accumulator like a partial and every contributor folds a share later.
+      const bool coop_t = P.coop && (partial || npeer > 0);
+      const bool publish = partial || coop_t;
+      const int fold_n = coop_t ? 0 : npeer;  // peers this owner folds itself
+      if (fold_n > 0) {
         if (lane == 0)
-          for (int p = 1; p <= npeer; ++p) wait_flag(P, P.flags + fidx(s.peer(tile, u, p)));
+          for (int p = 1; p <= fold_n; ++p) wait_flag(P, P.flags + fidx(s.peer(tile, u, p)));
         __syncwarp();
       }
       if (ev) ev[kEvWaitEnd] = ptx::globaltimer();
-      float* my_slab = partial ? partials + fidx(u) * static_cast<int64_t>(SLAB_ELEMS) : nullptr;
+      const int64_t my_idx = partial ? fidx(u) : own_base + fidx(u);
+      float* my_slab = publish ? slab(my_idx) : nullptr;
       // 64 columns (two 32-column chunks) per step: one tcgen05.ld.x64, 16 float4
       // of peer slab in flight per thread, two 32x32 TMA-store boxes.
-      const int c_lo = static_cast<int>((warp - 2) / 4) * (EPI_COLS / 32);
 #pragma unroll 1
       for (int c = c_lo; c < (orphan ? c_lo : c_lo + EPI_COLS / 32); c += 2) {
         float v[64];
         ptx::tmem_ld64(tsrc + c * 32, v);
-        if (partial) {
+        if (publish) {
 #pragma unroll
           for (int j = 0; j < 16; ++j)
             ptx::st_cg_f4(slab_ptr(my_slab, c + j / 8, j % 8, row),
@@ -330,8 +438,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         } else {
           // Owner fold: own accumulator, then peers in ascending id (executor.hpp:165-172).
 #pragma unroll 1
-          for (int p = 1; p <= npeer; ++p) {
-            float* ps = partials + fidx(s.peer(tile, u, p)) * static_cast<int64_t>(SLAB_ELEMS);
+          for (int p = 1; p <= fold_n; ++p) {
+            float* ps = slab(fidx(s.peer(tile, u, p)));
             float4 w[16];
 #pragma unroll
             for (int j = 0; j < 16; ++j) w[j] = ptx::ld_cg_f4(slab_ptr(ps, c + j / 8, j % 8, row));
@@ -350,32 +458,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               for (int j = 0; j < 16; ++j) ptx::discard_l2(slab_ptr(ps, c + j / 8, j % 8, row));
             }
           }
-          // Stage each 32-column half through a ring of EPI_BUFS swizzled smem boxes
-          // (16-B chunk j of row r at j ^ (r % 8)); EPI_BUFS - 1 TMA stores stay in
-          // flight while the next box is written.
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            float* buf = stage_buf + (nstores % EPI_BUFS) * (EPI_BUF_BYTES / 4);
-            if (nstores >= EPI_BUFS) {
-              if (lane == 0) ptx::tma_store_wait_read<EPI_BUFS - 1>();
-              __syncwarp();
-            }
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              const int jj = j ^ static_cast<int>(lane & 7);
-              *reinterpret_cast<float4*>(buf + lane * 32 + jj * 4) =
-                  make_float4(v[32 * h + 4 * j], v[32 * h + 4 * j + 1], v[32 * h + 4 * j + 2],
-                              v[32 * h + 4 * j + 3]);
-            }
-            ptx::fence_proxy_async_smem();
-            __syncwarp();
-            if (lane == 0) {
-              ptx::tma_store_2d_hint(&tmC, buf, n0 + (c + h) * 32, m0 + static_cast<int32_t>(q * 32),
-                                     pol_c);
-              ptx::tma_store_commit();
-            }
-            ++nstores;
-          }
+          store_box(v, n0, m0, c);
+          store_box(v + 32, n0, m0, c + 1);
         }
       }
       // Accumulator drained: hand the TMEM buffer back to the (leader's) MMA warp.
@@ -385,14 +469,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if constexpr (CG == 1) ptx::mbar_arrive(&tempty_bar[acc]);
         else mbar_arrive_remote(mapa(&tempty_bar[acc], 0));
       }
-      if (partial && !orphan) {
+      if (publish && !orphan) {
         __threadfence();
         ptx::named_bar_sync(1, 32 * EPI_WARPS);
         if (leader) {
-          signal_flag(P, P.flags + fidx(u));
-          if (P.trace && rank == 0) atomicAdd(P.trace + 4 * s.total_tiles + u, 1);
+          signal_flag(P, P.flags + my_idx);
+          if (P.trace && rank == 0 && partial) atomicAdd(P.trace + 4 * s.total_tiles + u, 1);
         }
-      } else if (!partial) {
+      }
+      if (!partial) {
         if (P.c_done) {  // this warp's rows of the tile are in HBM: count them for copy-out
           if (lane == 0) {
             ptx::tma_store_wait_all<0>();
@@ -402,10 +487,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
           __syncwarp();
         }
-        if (npeer > 0) {
+        if (fold_n > 0) {
           ptx::named_bar_sync(1, 32 * EPI_WARPS);
           if (leader)  // every epilogue warp has read the slabs: re-arm the flags
-            for (int p = 1; p <= npeer; ++p) ptx::st_relaxed(P.flags + fidx(s.peer(tile, u, p)), 0);
+            for (int p = 1; p <= fold_n; ++p) ptx::st_relaxed(P.flags + fidx(s.peer(tile, u, p)), 0);
         }
         if (leader && P.trace && rank == 0) {
           int* t = P.trace + 4 * tile;
@@ -425,6 +510,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
+      // Cooperative: shared tiles are folded once the unit has published all of
+      // its segments (at most its first and its last), so no fold ever waits
+      // behind this unit's own later mainloop work.
+      if (coop_t && !orphan) (npend++ == 0 ? pend0 : pend1) = tile;
+      if (npend > 0) {
+        int64_t b, e;
+        s.range(u, &b, &e);
+        if (tile * s.ipt + le == e) {
+          if (npend > 0) coop_fold(u, pend0);
+          if (npend > 1) coop_fold(u, pend1);
+          if (ev && npend) ev[kEvDone] = ptx::globaltimer();
+          npend = 0;
+        }
+      }
     }, P.sk_first);
     if (lane == 0) ptx::tma_store_wait_all<0>();
     __syncwarp();

@@ -15,12 +15,22 @@ namespace skb200 {
 //   [256, 256 + flag_bytes)    int32 flags, one per (slab, cta rank), zero between launches
 //   [partials_off, ...)        fixup slabs: num_slabs * ranks * slab_elems accumulators
 //   [table_off, total)         explicit schedules only: ranges, peer offsets, peer ids (int64)
+//
+// Cooperative fixup (KernelParams::coop, balanced strategies on the 16-bit
+// kernels): every balanced unit may publish two slabs, its first segment's
+// partial (slab/flag index slab_of(u) * ranks + rank, as in the owner-fold
+// protocol) and, as a tile owner, its last segment's accumulator (index
+// num_slabs * ranks + the same); then one done counter per (balanced-region
+// tile, rank) at flag index 2 * num_slabs * ranks + (tile - first tile) * ranks + rank.
 struct WorkspaceLayout {
   size_t flags_off = 256, flag_bytes = 0, partials_off = 0, table_off = 0, total = 0;
   static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
-  void compute(int64_t num_slabs, int ranks, size_t slab_bytes, size_t table_bytes = 0) {
+  void compute(int64_t num_slabs, int ranks, size_t slab_bytes, size_t table_bytes = 0,
+               int64_t coop_tiles = -1) {
+    const int64_t extra = coop_tiles >= 0 ? num_slabs * ranks + coop_tiles * ranks : 0;
+    if (coop_tiles >= 0) num_slabs *= 2;
     flags_off = 256;
-    flag_bytes = align256(sizeof(int) * static_cast<size_t>(num_slabs * ranks + 1));
+    flag_bytes = align256(sizeof(int) * static_cast<size_t>(num_slabs * ranks + extra + 1));
     partials_off = flags_off + flag_bytes;
     table_off = align256(partials_off + static_cast<size_t>(num_slabs * ranks) * slab_bytes);
     total = table_bytes ? table_off + table_bytes
@@ -66,6 +76,12 @@ struct KernelParams {
   // persistent CTA (pair) among those of its die, -1 unknown.  die_n = CTAs
   // (pairs) per die.  Only set for a full persistent grid on a probed device.
   int32_t die_aware;
+  // Cooperative fixup: each balanced unit runs alone on its CTA (all of them
+  // co-resident), so every contributor of a shared tile publishes its
+  // accumulator and then folds 1/ncontrib of the tile's columns from all
+  // slabs in the reference's order (owner first, peers ascending), instead of
+  // the owner folding every peer slab alone (per-SM bandwidth-bound).
+  int32_t coop;
   int32_t die_n[2];
   int16_t die_tab[kMaxSms];
 };

@@ -357,6 +357,33 @@ sk_status kernel_blocking(Kernel k, sk_blocking* out) {
 
 int kernel_ranks(Kernel k) { return k == Kernel::F16_2SM ? 2 : 1; }
 
+// Mean number of contributing units over the balanced region's shared tiles
+// (tiles with more than one contributor); 0 when none is shared.
+double mean_contributors(const Schedule& s) {
+  // units of >= ipt/4 iterations give tiles at most ~5 contributors: skip the
+  // scan (it then only runs for schedules with few tiles, g <= p units)
+  if (s.bal.q * 4 >= s.ipt) return 0.0;
+  int64_t shared = 0, sum = 0;
+  for (int64_t t = s.bal.begin / s.ipt; t < s.total_tiles; ++t) {
+    int64_t owner, last;
+    s.peers(t, &owner, &last);
+    if (last > owner) {
+      ++shared;
+      sum += last - owner + 1;
+    }
+  }
+  return shared ? static_cast<double>(sum) / static_cast<double>(shared) : 0.0;
+}
+
+// Balanced-region tiles the cooperative fixup keeps a done counter for, or -1
+// when the schedule/kernel never uses it (the workspace is sized for it
+// whenever the 16-bit kernels run a balanced schedule).
+int64_t coop_tiles(Kernel k, const Schedule& s) {
+  if (k == Kernel::F64 || s.bal.count == 0 || s.strategy == kFixedSplit || s.strategy == kExplicit)
+    return -1;
+  return s.total_tiles - s.bal.begin / s.ipt;
+}
+
 size_t kernel_slab_bytes(Kernel k) {
   switch (k) {
     case Kernel::F16_1SM: return f16_slab_bytes();
@@ -573,7 +600,7 @@ sk_status sk_workspace_size(const sk_gemm_desc* d, size_t* bytes) {
   if (st) return st;
   WorkspaceLayout L;
   L.compute(s.num_slabs, kernel_ranks(k), kernel_slab_bytes(k),
-            s.strategy == kExplicit ? g_xt.bytes() : 0);
+            s.strategy == kExplicit ? g_xt.bytes() : 0, coop_tiles(k, s));
   if (bytes) *bytes = L.total;
   return SK_OK;
 }
@@ -682,7 +709,8 @@ sk_status gemm_impl(const sk_gemm_desc* d, void* ws, size_t ws_bytes, cudaStream
     return fail(SK_EUNSUPPORTED, "leading dimensions must be multiples of 16 bytes (TMA)");
   const bool xp = s.strategy == kExplicit;
   WorkspaceLayout L;
-  L.compute(s.num_slabs, kernel_ranks(kern), kernel_slab_bytes(kern), xp ? g_xt.bytes() : 0);
+  L.compute(s.num_slabs, kernel_ranks(kern), kernel_slab_bytes(kern), xp ? g_xt.bytes() : 0,
+            coop_tiles(kern, s));
   if (!ws || ws_bytes < L.total)
     return fail(SK_EINVAL, "workspace of %zu bytes < required %zu", ws_bytes, L.total);
 
@@ -749,6 +777,20 @@ sk_status gemm_impl(const sk_gemm_desc* d, void* ws, size_t ws_bytes, cudaStream
   // Die-aware data-parallel phase: needs every SM (pair) in the persistent grid,
   // so each die's lane ranks are dense (dp_lane); the rasterised DP order is
   // otherwise unchanged.
+  // Cooperative fixup when every balanced unit has a CTA of its own (all of
+  // them run concurrently, so contributors can wait on each other); the
+  // transfer-pipelined sk_execute path keeps owner folds (its per-row store
+  // counts assume one storing CTA per tile).
+  // Only worth it when tiles have many contributors: measured on B200
+  // (profiles/r01/coop_fixup.txt) it wins from ~8 contributors per shared
+  // tile (768^2 x 16384: +22 %, 512^2 x 65536: +50 %) and loses below (the
+  // owner's serial fold of a few slabs is cheaper than every contributor
+  // publishing and folding after its last segment).
+  P.coop = 0;
+  if (coop_tiles(kern, s) >= 0 && s.bal.count <= P.num_ctas && !a_ready && !c_done) {
+    P.coop = mean_contributors(s) >= 8.0 ? 1 : 0;
+    if (const char* e = getenv("SKB200_COOP")) P.coop = atoi(e) != 0;
+  }
   P.die_aware = 0;
   if ((kern == Kernel::F16_1SM || kern == Kernel::F16_2SM) && s.dp_tiles > 0 &&
       P.num_ctas == info.sms / P.ranks && !a_ready)
