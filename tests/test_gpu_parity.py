@@ -469,3 +469,37 @@ def test_die_aware_lanes_bit_exact(sk, torch_cuda, monkeypatch, var):
             out.append(C)
         assert torch.equal(out[0], out[1])
         assert torch.equal(out[1].double().sum(1), rows)
+
+
+# ---------------------------------------------------------------- cooperative fixup
+@pytest.mark.parametrize("var", VARIANTS)
+@pytest.mark.parametrize("shape,g", [((256, 512, 16384), 74), ((512, 512, 8192), 48),
+                                     ((384, 640, 6000), 60), ((256, 256, 4096), 37)])
+def test_cooperative_fixup_bit_exact(sk, port, torch_cuda, monkeypatch, shape, g, var):
+    """Deep-k, few-tile Stream-K schedules (>= 8 contributors per tile) take the
+    cooperative fixup: integer-valued C bit-exact vs the oracle, and float C
+    bit-identical to the owner-fold protocol (same fold order)."""
+    torch = torch_cuda
+    m, n, k = shape
+    V = variant(sk, var)
+    blk = sk.kernel_blocking(sk.DType.BFloat16, V)
+    a = sk.stream_k(sk.GemmProblem(m, n, k), blk, g)
+    Ai, Bi = int_operands(port, m, n, k, 77 + k)
+    want = port.execute("stream_k", g, Ai, Bi, blk.blk_m, blk.blk_n, blk.blk_k).astype(np.float32)
+    rng = np.random.default_rng(k)
+    Af = to_bf16_f32(rng.uniform(-1, 1, (m, k)).astype(np.float32))
+    Bf = to_bf16_f32(rng.uniform(-1, 1, (k, n)).astype(np.float32))
+    outs = {}
+    for coop in ("1", "0"):
+        monkeypatch.setenv("SKB200_COOP", coop)
+        gemm = sk.Gemm(a, variant=V)
+        for name, (X, Y) in (("int", (Ai, Bi)), ("float", (Af, Bf))):
+            A = torch.from_numpy(X.astype(np.float32)).cuda().to(torch.bfloat16)
+            B = torch.from_numpy(Y.astype(np.float32)).cuda().to(torch.bfloat16)
+            C = torch.full((m, n), float("nan"), device="cuda")
+            for _ in range(2):  # second launch: flags re-armed by the first
+                gemm.run(A, B, C)
+            gemm.check()
+            outs[coop, name] = C.cpu().numpy()
+    assert np.array_equal(outs["1", "int"], want)
+    assert np.array_equal(outs["1", "float"], outs["0", "float"])
