@@ -95,6 +95,13 @@ struct Schedule {
   int64_t split = 1, ips = 1;
   // fixup slabs: which units emit a partial, compact slab index
   int64_t num_slabs = 0;
+  // Tile id -> C block (tile_rc).  1: row-major, the reference's
+  // executor.hpp:69-70.  G > 1: ids run through groups of G tile rows,
+  // column-major inside a group (the last group may be shorter), so every
+  // contiguous id range -- a wave of data-parallel tiles, a hybrid's trailing
+  // Stream-K region -- covers a compact block of C.  Ids, ranges, owners and
+  // peers are untouched; only which block of C an id denotes changes.
+  int64_t tile_group = 1;
   // kExplicit: [g][2] ranges and per-tile ascending peer ids (CSR); the first
   // peer of a tile is its starter when that range covers local k = 0.
   const int64_t* xr = nullptr;
@@ -179,6 +186,19 @@ struct Schedule {
       default:
         return 1;
     }
+  }
+
+  SK_HD void tile_rc(int64_t tile, int64_t* r, int64_t* c) const {
+    if (tile_group <= 1) {
+      *r = tile / tiles_n;
+      *c = tile % tiles_n;
+      return;
+    }
+    const int64_t span = tile_group * tiles_n;
+    const int64_t g = tile / span, w = tile - g * span;
+    const int64_t h = imin(tile_group, tiles_m - g * tile_group);
+    *c = w / h;
+    *r = g * tile_group + (w - *c * h);
   }
 
   // Range of logical CTA u in [0, grid_size).

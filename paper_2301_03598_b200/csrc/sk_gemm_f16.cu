@@ -202,13 +202,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       uint32_t stage = 0, phase = 0;
       for_each_segment(s, cta, P.num_ctas, dp_lane, P.raster_rows,
                        [&](int64_t u, int64_t tile, int64_t lb, int64_t le) {
-        const int32_t m0 = static_cast<int32_t>((tile / s.tiles_n) * (ROWS * CG) + rank * ROWS);
-        const int32_t n0 = static_cast<int32_t>((tile % s.tiles_n) * BN + rank * K::B_COLS);
+        int64_t tr, tc;
+        s.tile_rc(tile, &tr, &tc);
+        const int32_t m0 = static_cast<int32_t>(tr * (ROWS * CG) + rank * ROWS);
+        const int32_t n0 = static_cast<int32_t>(tc * BN + rank * K::B_COLS);
         // B panels stream through a data-parallel wave but are revisited at
         // unrelated k offsets by Stream-K units: separate L2 priorities.
         const bool sk_unit = s.strategy == kFixedSplit || s.bal.contains_id(u);
         const uint64_t pol_b = sk_unit ? pol_b_sk : pol_b_dp;
-        if (P.a_ready) wait_flag(P, P.a_ready + tile / s.tiles_n);  // row block of A in HBM
+        if (P.a_ready) wait_flag(P, P.a_ready + tr);  // row block of A in HBM
         // k order of a balanced unit's segments (P.k_align): see k_block_of.
         int64_t rot = -1;
         if (P.k_align && sk_unit && s.strategy != kFixedSplit) {
@@ -333,8 +335,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       s.peers(tile, &owner, &last);
       const int ncon = static_cast<int>(last - owner + 1);
       const int idx = static_cast<int>(u - owner);
-      const int32_t m0 = static_cast<int32_t>((tile / s.tiles_n) * (ROWS * CG) + rank * ROWS);
-      const int32_t n0 = static_cast<int32_t>((tile % s.tiles_n) * BN);
+      int64_t tr, tc;
+      s.tile_rc(tile, &tr, &tc);
+      const int32_t m0 = static_cast<int32_t>(tr * (ROWS * CG) + rank * ROWS);
+      const int32_t n0 = static_cast<int32_t>(tc * BN);
       if (idx < EPI_COLS / 32) {  // else: no chunk to fold (more contributors than chunks)
         if (lane == 0) {
           wait_flag(P, P.flags + own_base + fidx(owner));
@@ -406,8 +410,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       long long* ev = (leader && rank == 0) ? event_slot(P, u, tile) : nullptr;
       if (ev) ev[kEvMacEnd] = ptx::globaltimer();
       const uint32_t tsrc = tmem_base + acc * BN + ((q * 32) << 16);
-      const int32_t m0 = static_cast<int32_t>((tile / s.tiles_n) * (ROWS * CG) + rank * ROWS);
-      const int32_t n0 = static_cast<int32_t>((tile % s.tiles_n) * BN);
+      int64_t tr, tc;
+      s.tile_rc(tile, &tr, &tc);
+      const int32_t m0 = static_cast<int32_t>(tr * (ROWS * CG) + rank * ROWS);
+      const int32_t n0 = static_cast<int32_t>(tc * BN);
       const bool partial = lb != 0;  // not the tile starter (executor.hpp:160)
       const bool orphan = partial && s.orphan(tile);  // explicit table: nobody folds it
       const int npeer = (!partial && (le < s.ipt || s.strategy == kExplicit)) ? s.npeers(tile, u) : 0;
@@ -483,7 +489,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             ptx::tma_store_wait_all<0>();
             ptx::fence_proxy_async_global();
             __threadfence_system();
-            atomicAdd(P.c_done + tile / s.tiles_n, 1);
+            atomicAdd(P.c_done + tr, 1);
           }
           __syncwarp();
         }

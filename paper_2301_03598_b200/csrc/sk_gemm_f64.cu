@@ -95,9 +95,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
       uint32_t stage = 0, phase = 0;
       for_each_segment(s, cta, P.num_ctas, P.raster_rows,
                        [&](int64_t, int64_t tile, int64_t lb, int64_t le) {
-        const int32_t m0 = static_cast<int32_t>((tile / s.tiles_n) * BM);
-        const int32_t n0 = static_cast<int32_t>((tile % s.tiles_n) * BN);
-        if (P.a_ready) wait_flag(P, P.a_ready + tile / s.tiles_n);  // row block of A in HBM
+        int64_t tr, tc;
+        s.tile_rc(tile, &tr, &tc);
+        const int32_t m0 = static_cast<int32_t>(tr * BM);
+        const int32_t n0 = static_cast<int32_t>(tc * BN);
+        if (P.a_ready) wait_flag(P, P.a_ready + tr);  // row block of A in HBM
         for (int64_t kb = lb; kb < le; ++kb) {
           ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
           ptx::mbar_expect_tx(&full_bar[stage], STAGE_BYTES);
@@ -224,7 +226,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
       t[3] = npeer;
     }
     // Clamped store of the owner's tile (executor.hpp:175-181).
-    const int64_t m0 = (tile / s.tiles_n) * BM, n0 = (tile % s.tiles_n) * BN;
+    int64_t tr, tc;
+    s.tile_rc(tile, &tr, &tc);
+    const int64_t m0 = tr * BM, n0 = tc * BN;
 #pragma unroll
     for (int i = 0; i < 2; ++i)
 #pragma unroll
@@ -244,7 +248,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
     if (P.c_done) {  // the tile is in HBM: count it for copy-out
       __threadfence_system();
       ptx::named_bar_sync(1, 128);
-      if (tid == 0) atomicAdd(P.c_done + tile / s.tiles_n, 1);
+      if (tid == 0) atomicAdd(P.c_done + tr, 1);
     }
     if (ev) {
       if (npeer == 0) ev[kEvWaitEnd] = ev[kEvMacEnd];

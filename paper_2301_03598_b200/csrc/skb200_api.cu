@@ -751,6 +751,24 @@ sk_status gemm_impl(const sk_gemm_desc* d, void* ws, size_t ws_bytes, cudaStream
   // kept near 32 MB so they stay L2-resident while B streams through; measured
   // best at 8192^3: 16 rows (1-SM), 8 rows (2-SM) (profiles/r01/raster_rows.txt).
   P.raster_rows = raster > 0 ? raster : raster_rows_for(d);
+  // Grouped tile ids (Schedule::tile_rc): the same G-row groups now also
+  // decide which block of C each tile id denotes, so a hybrid's trailing
+  // Stream-K region is a compact 8 x 17 block at 8192^3 instead of a
+  // 4.25 x 32 band (B panels fit L2): two_tile_sk_dp 1482 -> 1505 TFLOP/s,
+  // data-parallel unchanged (profiles/r01/tile_group.txt).  The transfer-
+  // pipelined sk_execute keeps row-major ids (its copies go by rows of C), and
+  // so do explicit tables: with gaps or orphan tiles, which block of C stays
+  // zero is observable (the reference's row-major id).  The DMMA kernel keeps
+  // its raster (it is compute-bound, insensitive to L2 placement).
+  // SKB200_TILE_GROUP=1 restores the reference's row-major tile ids.
+  if (!a_ready && !xp && kern != Kernel::F64) {
+    int64_t group = P.raster_rows;
+    if (const char* e = getenv("SKB200_TILE_GROUP")) group = std::max(1, atoi(e));
+    if (group > 1) {
+      P.s.tile_group = group;
+      P.raster_rows = 1;  // the id order already is the raster
+    }
+  }
   // L2 eviction priorities {A loads, B loads, C stores}: 0 normal, 1 first, 2 last.
   // A panels are re-read across a raster group's waves (keep), B panels stream
   // through a wave and C is written once (evict first); measured +4 % at 8192^3

@@ -31,6 +31,8 @@ def main():
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--rounds", type=int, default=4)
+    ap.add_argument("--no-check", action="store_true",
+                    help="arms may legitimately differ in float rounding (e.g. k order)")
     ap.add_argument("--cool", type=float, default=1.0, help="idle seconds before each measurement "
                     "(every arm then starts from the same power/thermal state)")
     args = ap.parse_args()
@@ -77,7 +79,7 @@ def main():
             cs = float(C.double().sum())
             if ref is None:
                 ref = cs
-            elif cs != ref:  # deterministic: bit-identical C across arms
+            elif cs != ref and not args.no_check:  # deterministic: bit-identical C across arms
                 raise SystemExit(f"checksum mismatch for {env}: {cs} vs {ref}")
     print(json.dumps({"shape": [m, n, k], "strategy": args.strategy,
                       "arms": [{"env": env, "tflops": r, "median": float(np.median(r))}
