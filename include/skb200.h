@@ -181,6 +181,10 @@ typedef struct sk_cost_params {
   double e, a, b, c, d, s;
   double margin;
   double fit_residual;
+  /* > 0: the kernel's cooperative fixup (g <= p, tiles of >= 8 contributors)
+   * costs like coop_peers serial peer folds, not peers - 1 (0 = the
+   * reference's model, an owner folding every peer). */
+  double coop_peers;
 } sk_cost_params;
 /* B200-calibrated constants for a kernel family. */
 sk_status sk_default_cost_params(sk_dtype ab_type, sk_variant variant, sk_cost_params* out);

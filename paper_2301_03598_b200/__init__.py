@@ -448,7 +448,7 @@ class CostParams(C.Structure):
     `margin` = minimum predicted gain before leaving data-parallel."""
     _fields_ = [("e", C.c_double), ("a", C.c_double), ("b", C.c_double), ("c", C.c_double),
                 ("d", C.c_double), ("s", C.c_double), ("margin", C.c_double),
-                ("fit_residual", C.c_double)]
+                ("fit_residual", C.c_double), ("coop_peers", C.c_double)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -477,14 +477,16 @@ def select_grid_size(params: CostParams, grid: "TileGrid", p: int) -> int:
     return out.value
 
 
-def calibrate(samples, p: int, margin: float = 0.15) -> CostParams:
-    """NNLS fit from [(TileGrid, g, time_us), ...] (costmodel.cpp:142-225)."""
+def calibrate(samples, p: int, margin: float = 0.15, coop_peers: float = 0.0) -> CostParams:
+    """NNLS fit from [(TileGrid, g, time_us), ...] (costmodel.cpp:142-225);
+    coop_peers > 0 models the kernel's cooperative fixup (see sk_cost_params)."""
     n = len(samples)
     grids = (sk_tile_grid_t * n)(*[s[0]._c() for s in samples])
     gs = np.array([s[1] for s in samples], np.int64)
     ts = np.array([s[2] for s in samples], np.float64)
     out = CostParams()
     out.margin = margin
+    out.coop_peers = coop_peers
     _check(lib().sk_calibrate(grids, gs.ctypes.data_as(C.c_void_p), ts.ctypes.data_as(C.c_void_p),
                               n, p, C.byref(out)), "calibrate")
     return out

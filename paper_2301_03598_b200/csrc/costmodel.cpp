@@ -30,9 +30,14 @@ constexpr int kF = 6;
 
 int64_t cdiv(int64_t x, int64_t y) { return (x + y - 1) / y; }
 
-void features(const sk_tile_grid_t& g, int64_t gs, int64_t p, double f[kF]) {
+void features(const sk_tile_grid_t& g, int64_t gs, int64_t p, double f[kF], double coop_peers = 0.0) {
   const int64_t ipc = cdiv(g.total_iters, gs);
   const int64_t peers = cdiv(g.iters_per_tile, ipc);
+  // The kernel's cooperative fixup (one unit per CTA, tiles of >= 8
+  // contributors, skb200_api.cu) spreads the fold over all contributors.
+  const bool coop = coop_peers > 0.0 && gs <= p && ipc * 4 < g.iters_per_tile && peers + 1 >= 8;
+  const double fold_peers = coop ? std::min(coop_peers, static_cast<double>(peers - 1))
+                                 : static_cast<double>(peers - 1);
   const int64_t segs = ipc % g.iters_per_tile == 0 ? ipc / g.iters_per_tile
                                                    : cdiv(ipc, g.iters_per_tile) + 1;
   const double w = static_cast<double>(cdiv(gs, p));
@@ -40,7 +45,7 @@ void features(const sk_tile_grid_t& g, int64_t gs, int64_t p, double f[kF]) {
   f[1] = w;
   f[2] = w * (peers > 1 ? 1.0 : 0.0);
   f[3] = w * static_cast<double>(ipc);
-  f[4] = w * static_cast<double>(peers - 1);
+  f[4] = w * fold_peers;
   f[5] = w * static_cast<double>(segs);
 }
 
@@ -145,7 +150,7 @@ sk_status sk_predict_time(const sk_cost_params* c, const sk_tile_grid_t* g, int6
                           double* out) {
   if (!c || !valid_grid(g) || gs < 1 || p < 1 || !out) return SK_EINVAL;
   double f[kF];
-  features(*g, gs, p, f);
+  features(*g, gs, p, f, c->coop_peers);
   *out = dot(*c, f);
   return SK_OK;
 }
@@ -193,7 +198,7 @@ sk_status sk_predict_schedule(const sk_cost_params* c, const sk_tile_grid_t* g, 
       sk_region.total_tiles = t - d;
       sk_region.total_iters = (t - d) * g->iters_per_tile;
       double f[kF];
-      features(sk_region, param, p, f);
+      features(sk_region, param, p, f, c->coop_peers);
       double t_sk = dot(*c, f);
       const double dp_waves = static_cast<double>(cdiv(d, p));
       *out = t_sk + dp_waves * (c->a + c->c * static_cast<double>(g->iters_per_tile) + c->s);
@@ -254,7 +259,7 @@ sk_status sk_calibrate(const sk_tile_grid_t* grids, const int64_t* gs, const dou
   for (int64_t i = 0; i < n; ++i) {
     if (!valid_grid(&grids[i]) || gs[i] < 1 || !(times[i] > 0)) return SK_EINVAL;
     double f[kF];
-    features(grids[i], gs[i], p, f);
+    features(grids[i], gs[i], p, f, out->coop_peers);
     for (int j = 0; j < kF; ++j) A[static_cast<size_t>(i) * kF + j] = f[j] / times[i];
     b[static_cast<size_t>(i)] = 1.0;  // relative error: (pred - t) / t
   }
@@ -267,6 +272,7 @@ sk_status sk_calibrate(const sk_tile_grid_t* grids, const int64_t* gs, const dou
     res += r * r;
   }
   const double margin = out->margin;
+  const double coop_peers = out->coop_peers;
   out->e = x[0];
   out->a = x[1];
   out->b = x[2];
@@ -274,6 +280,7 @@ sk_status sk_calibrate(const sk_tile_grid_t* grids, const int64_t* gs, const dou
   out->d = x[4];
   out->s = x[5];
   out->margin = margin;
+  out->coop_peers = coop_peers;
   out->fit_residual = std::sqrt(res / static_cast<double>(n));  // RMS relative error
   return SK_OK;
 }
@@ -281,6 +288,10 @@ sk_status sk_calibrate(const sk_tile_grid_t* grids, const int64_t* gs, const dou
 // B200 constants (microseconds), fitted with sk_calibrate on samples measured
 // by `python -m paper_2301_03598_b200.sweep --calibrate` (corpus seed 1,
 // disjoint from the seed-0 evaluation corpus); see profiles/r01/costmodel.json.
+// Cooperative fold cost in serial-peer-fold units: measured 3.7 (768^2 x 16384,
+// 9 contributors) and 4.7 (512^2 x 65536, 19) on B200 (profiles/r01/coop_fixup.txt).
+constexpr double kCoopPeers = 4.0;
+
 sk_status sk_default_cost_params(sk_dtype ab_type, sk_variant variant, sk_cost_params* out) {
   if (!out) return SK_EINVAL;
   if (ab_type != SK_BFLOAT16 && ab_type != SK_FLOAT16 && ab_type != SK_FLOAT64) return SK_EINVAL;
@@ -288,9 +299,9 @@ sk_status sk_default_cost_params(sk_dtype ab_type, sk_variant variant, sk_cost_p
   if (ab_type == SK_FLOAT64) {
     c = {0.0, 5.2158, 0.0, 0.71323, 0.95141, 0.62478, 0.3, 0.0};  // costmodel_fp64.json
   } else if (variant == SK_VARIANT_2SM || variant == SK_VARIANT_AUTO) {
-    c = {3.9049, 0.9955, 0.4063, 0.3098, 2.3291, 3.3913, 0.2, 0.0};
+    c = {3.9049, 0.9955, 0.4063, 0.3098, 2.3291, 3.3913, 0.2, 0.0, kCoopPeers};
   } else {
-    c = {4.2166, 0.24668, 1.8380, 0.42998, 2.6520, 2.8518, 0.2, 0.0};  // costmodel_1sm.json
+    c = {4.2166, 0.24668, 1.8380, 0.42998, 2.6520, 2.8518, 0.2, 0.0, kCoopPeers};  // costmodel_1sm.json
   }
   *out = c;
   return SK_OK;

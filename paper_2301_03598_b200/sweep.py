@@ -194,7 +194,8 @@ def fit_cost_model(rows, p):
             grid = sk.TileGrid(r["tiles_m"], r["tiles_n"], r["t"], r["iters_per_tile"],
                                r["t"] * r["iters_per_tile"])
             samples.append((grid, r["g"], r["time_us"]))
-    params = sk.calibrate(samples, p)
+    # the 16-bit kernels' cooperative fixup is part of what was measured
+    params = sk.calibrate(samples, p, coop_peers=sk.default_cost_params().coop_peers)
     return params, len(samples)
 
 

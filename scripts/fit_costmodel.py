@@ -35,7 +35,8 @@ def main():
             t, ipt = int(r["t"]), int(r["iters_per_tile"])
             grid = sk.TileGrid(int(r["tiles_m"]), int(r["tiles_n"]), t, ipt, t * ipt)
             samples.append((grid, int(r["g"]), float(r["time_us"]), r))
-    params = sk.calibrate([s[:3] for s in samples], a.p, a.margin)
+    params = sk.calibrate([s[:3] for s in samples], a.p, a.margin,
+                          coop_peers=sk.default_cost_params().coop_peers)
     by = collections.defaultdict(list)
     for grid, g, t, r in samples:
         by[(r["m"], r["n"], r["k"])].append((sk.predict_time(params, grid, g, a.p), t, r["strategy"]))
