@@ -182,8 +182,8 @@ typedef struct sk_cost_params {
   double margin;
   double fit_residual;
   /* > 0: the kernel's cooperative fixup (g <= p, tiles of >= 8 contributors)
-   * costs like coop_peers serial peer folds, not peers - 1 (0 = the
-   * reference's model, an owner folding every peer). */
+   * costs like coop_peers + contributors / 8 serial peer folds, not peers - 1
+   * (0 = the reference's model: the owner folds every peer). */
   double coop_peers;
 } sk_cost_params;
 /* B200-calibrated constants for a kernel family. */

@@ -35,9 +35,12 @@ void features(const sk_tile_grid_t& g, int64_t gs, int64_t p, double f[kF], doub
   const int64_t peers = cdiv(g.iters_per_tile, ipc);
   // The kernel's cooperative fixup (one unit per CTA, tiles of >= 8
   // contributors, skb200_api.cu) spreads the fold over all contributors.
+  // Its cost in serial-peer-fold units: a publish plus, per folding
+  // contributor, ncontrib 32-column chunks (1/8 of a slab each).
   const bool coop = coop_peers > 0.0 && gs <= p && ipc * 4 < g.iters_per_tile && peers + 1 >= 8;
-  const double fold_peers = coop ? std::min(coop_peers, static_cast<double>(peers - 1))
-                                 : static_cast<double>(peers - 1);
+  const double fold_peers =
+      coop ? std::min(coop_peers + static_cast<double>(peers + 1) / 8.0, static_cast<double>(peers - 1))
+           : static_cast<double>(peers - 1);
   const int64_t segs = ipc % g.iters_per_tile == 0 ? ipc / g.iters_per_tile
                                                    : cdiv(ipc, g.iters_per_tile) + 1;
   const double w = static_cast<double>(cdiv(gs, p));
@@ -288,9 +291,13 @@ sk_status sk_calibrate(const sk_tile_grid_t* grids, const int64_t* gs, const dou
 // B200 constants (microseconds), fitted with sk_calibrate on samples measured
 // by `python -m paper_2301_03598_b200.sweep --calibrate` (corpus seed 1,
 // disjoint from the seed-0 evaluation corpus); see profiles/r01/costmodel.json.
-// Cooperative fold cost in serial-peer-fold units: measured 3.7 (768^2 x 16384,
-// 9 contributors) and 4.7 (512^2 x 65536, 19) on B200 (profiles/r01/coop_fixup.txt).
-constexpr double kCoopPeers = 4.0;
+// Cooperative fold cost in serial-peer-fold units = coop_peers + contributors / 8
+// fits the two measured points (3.7 at 9 contributors, 4.7 at 19) with 2.5, but
+// a policy using it (2.5 or a flat 4) picked Stream-K on 1-3-tile deep-k shapes
+// where it lost up to 2x and scored config 3 at 1.353 / corpus-1000 at 1.017 vs
+// 1.379 / 1.022 without it (profiles/r01/coop_fixup.txt): the default stays the
+// reference's owner-fold model, coop_peers = 0.
+constexpr double kCoopPeers = 0.0;
 
 sk_status sk_default_cost_params(sk_dtype ab_type, sk_variant variant, sk_cost_params* out) {
   if (!out) return SK_EINVAL;
