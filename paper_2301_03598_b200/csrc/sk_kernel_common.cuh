@@ -160,11 +160,11 @@ enum : int { kDpFirst = 0, kSkFirst = 1, kInterleaved = 2 };
 template <class F>
 SK_HD void for_each_segment(const Schedule& s, int64_t cta, int64_t P, const DpLane& lane,
                             int64_t raster_rows, F&& f, int order = kDpFirst) {
-  auto dp_phase = [&] {
+  auto dp_phase = [&]() __attribute__((always_inline)) {
     for (int64_t i = lane.first; i < lane.end; i += lane.step)
       run_unit(s, s.dp_id0 + raster_tile(s, i, raster_rows), f);
   };
-  auto desc_phase = [&](int64_t lo, int64_t hi) {
+  auto desc_phase = [&](int64_t lo, int64_t hi) __attribute__((always_inline)) {
     for (int64_t u = hi - 1 - cta; u >= lo; u -= P) run_unit(s, u, f);
   };
   if (s.strategy == kFixedSplit || s.strategy == kExplicit) {

@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--n", type=int, default=8192)
     ap.add_argument("--k", type=int, default=8192)
     ap.add_argument("--dtype", default="bf16")
+    ap.add_argument("--g", type=int, default=74, help="stream_k grid / hybrid p")
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--rounds", type=int, default=4)
@@ -39,17 +40,18 @@ def main():
     m, n, k = args.m, args.n, args.k
     ab = sk.DType.BFloat16 if args.dtype == "bf16" else sk.DType.Float16
     tdt = torch.bfloat16 if args.dtype == "bf16" else torch.float16
-    A = (torch.rand(m, k, device="cuda") * 2 - 1).to(tdt)
-    B = (torch.rand(k, n, device="cuda") * 2 - 1).to(tdt)
-    C = torch.empty(m, n, device="cuda", dtype=torch.float32)
+    pad = lambda x, q: (x + q - 1) // q * q  # noqa: E731  16-byte rows for TMA
+    A = (torch.rand(m, pad(k, 8), device="cuda") * 2 - 1).to(tdt)[:, :k]
+    B = (torch.rand(k, pad(n, 8), device="cuda") * 2 - 1).to(tdt)[:, :n]
+    C = torch.empty(m, pad(n, 4), device="cuda", dtype=torch.float32)[:, :n]
     blk = sk.kernel_blocking(ab, sk.Variant.TwoSM)
     prob = sk.GemmProblem(m, n, k)
     if args.strategy == "data_parallel":
         a = sk.data_parallel(prob, blk)
     elif args.strategy == "stream_k":
-        a = sk.stream_k(prob, blk, 74)
+        a = sk.stream_k(prob, blk, args.g)
     else:
-        a = sk.hybrid(prob, blk, 74, sk.HybridVariant.TwoTileSkDp)
+        a = sk.hybrid(prob, blk, args.g, sk.HybridVariant.TwoTileSkDp)
     g = sk.Gemm(a, ab, sk.Variant.TwoSM)
     stream = torch.cuda.current_stream()
     flops = 2.0 * m * n * k
