@@ -74,7 +74,13 @@ struct Region {
   SK_HD int64_t unit_of(int64_t j) const {
     const int64_t d = j - begin;
     const int64_t big = r * (q + 1);
+#if defined(__CUDA_ARCH__)  // < 2^31 on the device (see Schedule::tile_rc)
+    const uint32_t d32 = static_cast<uint32_t>(d), big32 = static_cast<uint32_t>(big);
+    const uint32_t q32 = static_cast<uint32_t>(q);
+    return first_id + (d32 < big32 ? d32 / (q32 + 1) : static_cast<uint32_t>(r) + (d32 - big32) / q32);
+#else
     return first_id + (d < big ? d / (q + 1) : r + (d - big) / q);
+#endif
   }
 };
 
@@ -188,7 +194,25 @@ struct Schedule {
     }
   }
 
+  // On the device every id and iteration is < 2^31 (sk_gemm rejects larger
+  // problems), so the divisions run in 32 bits: a 64-bit division is a
+  // ~100-instruction routine on the per-segment critical path.
   SK_HD void tile_rc(int64_t tile, int64_t* r, int64_t* c) const {
+#if defined(__CUDA_ARCH__)
+    const uint32_t t = static_cast<uint32_t>(tile), tn = static_cast<uint32_t>(tiles_n);
+    if (tile_group <= 1) {
+      const uint32_t q = t / tn;
+      *r = q;
+      *c = t - q * tn;
+      return;
+    }
+    const uint32_t G = static_cast<uint32_t>(tile_group), span = G * tn;
+    const uint32_t g = t / span, w = t - g * span;
+    const uint32_t h = min(G, static_cast<uint32_t>(tiles_m) - g * G);
+    const uint32_t cc = w / h;
+    *c = cc;
+    *r = g * G + (w - cc * h);
+#else
     if (tile_group <= 1) {
       *r = tile / tiles_n;
       *c = tile % tiles_n;
@@ -199,6 +223,7 @@ struct Schedule {
     const int64_t h = imin(tile_group, tiles_m - g * tile_group);
     *c = w / h;
     *r = g * tile_group + (w - *c * h);
+#endif
   }
 
   // Range of logical CTA u in [0, grid_size).

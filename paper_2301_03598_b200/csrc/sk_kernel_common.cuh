@@ -137,63 +137,119 @@ SK_HD int64_t raster_tile(const Schedule& s, int64_t i, int64_t rows) {
 // ids for TwoTileSkDp, below for DpOneTileSk).  Inside a unit, segments run in
 // ascending iteration order (executor.hpp:149-185).  Producer, MMA and epilogue
 // roles all walk this same sequence.
-#pragma nv_exec_check_disable
-template <class F>
-SK_HD void run_unit(const Schedule& s, int64_t u, F& f) {
-  int64_t b, e;
-  s.range(u, &b, &e);
-  int64_t it = b;
-  while (it < e) {
-    const int64_t tile = it / s.ipt;
-    const int64_t tb = tile * s.ipt;
-    const int64_t lb = it - tb;
-    const int64_t le = imin(e, tb + s.ipt) - tb;
-    f(u, tile, lb, le);
-    it = tb + s.ipt;
-  }
-}
-
 // Phase orders for TwoTileSkDp (KernelParams::sk_first):
 enum : int { kDpFirst = 0, kSkFirst = 1, kInterleaved = 2 };
+
+// The persistent CTA's segment sequence as an explicit iterator, so each role
+// (producer, MMA issuer, epilogue) has ONE copy of its per-segment body:
+//   SegmentIter it(s, cta, P, lane, raster_rows, order);
+//   int64_t u, tile, lb, le;
+//   while (it.next(s, &u, &tile, &lb, &le)) { ... }
+// Phases: up to two of {data-parallel slots of `lane` in the rasterised order,
+// balanced / fixed-split ids descending from hi - 1 - cta by P}; kInterleaved
+// puts the CTA's single balanced unit after `slot` of its data-parallel tiles.
+// The schedule is passed to every call rather than stored (a stored pointer to
+// the kernel parameter block would force a local-memory copy of it).
+struct SegmentIter {
+  enum : int { kNone = 0, kDp = 1, kDesc = 2 };
+  int64_t cta, P, raster;
+  DpLane lane;
+  int ph = 0, nph = 0;
+  int kind0 = kNone, kind1 = kNone;
+  int64_t lo = 0, hi = 0;     // kDesc id range
+  int64_t i = 0;              // current DP slot / descending id
+  bool fresh = true;          // phase not started yet
+  int64_t ins_unit = -1, ins_slot = -1, j = 0;  // kInterleaved: unit, slot, DP tiles so far
+  int64_t u = 0, it = 0, e = 0;
+
+  SK_HD SegmentIter(const Schedule& s, int64_t cta_, int64_t P_, const DpLane& lane_,
+                    int64_t raster_, int order)
+      : cta(cta_), P(P_), raster(raster_), lane(lane_) {
+    const bool two_tile_dp_first = s.dp_id0 > s.bal.first_id;
+    if (s.strategy == kFixedSplit || s.strategy == kExplicit) {
+      kind0 = kDesc, nph = 1, lo = 0, hi = s.grid_size;
+    } else if (s.bal.count == 0) {
+      kind0 = kDp, nph = 1;
+    } else {
+      lo = s.bal.first_id, hi = s.bal.first_id + s.bal.count;
+      if (two_tile_dp_first && order == kInterleaved && s.bal.count <= P_) {
+        // TwoTileSkDp with at most one balanced unit per CTA, staggered through
+        // the data-parallel waves: unit hi-1-cta runs after `slot` of this CTA's
+        // DP tiles, slot rising with cta, so a tile's peers (higher ids = lower
+        // cta) never run later than its owner.
+        kind0 = kDp, nph = 1;
+        const int64_t uu = hi - 1 - cta_;
+        const int64_t waves = (s.dp_tiles + P_ - 1) / P_;
+        if (uu >= lo) ins_unit = uu, ins_slot = cta_ * (waves + 1) / P_;
+      } else if (two_tile_dp_first && order == kDpFirst) {  // DP waves, then the SK region
+        kind0 = kDp, kind1 = kDesc, nph = 2;
+      } else {  // StreamK, DpOneTileSk, TwoTileSkDp SK-first (Fig. 4c)
+        kind0 = kDesc, kind1 = kDp, nph = 2;
+      }
+    }
+  }
+
+  // Next unit of the sequence into (u, it, e); false when exhausted.
+  SK_HD bool next_unit(const Schedule& s) {
+    while (ph < nph) {
+      if ((ph == 0 ? kind0 : kind1) == kDp) {
+        if (ins_unit >= 0 && j == ins_slot) {  // interleaved balanced unit, before DP tile j
+          const int64_t uu = ins_unit;
+          ins_unit = -1;
+          return load(s, uu);
+        }
+        i = fresh ? lane.first : i + lane.step;
+        fresh = false;
+        if (i < lane.end) {
+          ++j;
+          return load(s, s.dp_id0 + raster_tile(s, i, raster));
+        }
+        if (ins_unit >= 0) {  // its slot lies past this CTA's last DP tile
+          const int64_t uu = ins_unit;
+          ins_unit = -1;
+          return load(s, uu);
+        }
+      } else {
+        i = fresh ? hi - 1 - cta : i - P;
+        fresh = false;
+        if (i >= lo) return load(s, i);
+      }
+      ++ph;
+      fresh = true;
+    }
+    return false;
+  }
+  SK_HD bool load(const Schedule& s, int64_t unit) {
+    u = unit;
+    s.range(unit, &it, &e);
+    return true;
+  }
+  // Next tile segment: unit u, tile, local iterations [lb, le) (executor.hpp:149-185).
+  SK_HD bool next(const Schedule& s, int64_t* uo, int64_t* tile, int64_t* lb, int64_t* le) {
+    while (it >= e)
+      if (!next_unit(s)) return false;
+#if defined(__CUDA_ARCH__)  // ids and iterations < 2^31 on the device: 32-bit divide
+    const int64_t t = static_cast<uint32_t>(it) / static_cast<uint32_t>(s.ipt);
+#else
+    const int64_t t = it / s.ipt;
+#endif
+    const int64_t tb = t * s.ipt;
+    *uo = u;
+    *tile = t;
+    *lb = it - tb;
+    *le = imin(e, tb + s.ipt) - tb;
+    it = tb + s.ipt;
+    return true;
+  }
+};
 
 #pragma nv_exec_check_disable
 template <class F>
 SK_HD void for_each_segment(const Schedule& s, int64_t cta, int64_t P, const DpLane& lane,
                             int64_t raster_rows, F&& f, int order = kDpFirst) {
-  auto dp_phase = [&]() __attribute__((always_inline)) {
-    for (int64_t i = lane.first; i < lane.end; i += lane.step)
-      run_unit(s, s.dp_id0 + raster_tile(s, i, raster_rows), f);
-  };
-  auto desc_phase = [&](int64_t lo, int64_t hi) __attribute__((always_inline)) {
-    for (int64_t u = hi - 1 - cta; u >= lo; u -= P) run_unit(s, u, f);
-  };
-  if (s.strategy == kFixedSplit || s.strategy == kExplicit) {
-    desc_phase(0, s.grid_size);
-  } else if (s.bal.count == 0) {
-    dp_phase();
-  } else if (s.dp_id0 > s.bal.first_id && order == kInterleaved && s.bal.count <= P) {
-    // TwoTileSkDp with at most one balanced unit per CTA, staggered through the
-    // data-parallel waves: CTA `cta` runs unit hi-1-cta after `slot` of its own
-    // data-parallel tiles, slot rising with cta.  A tile's peers (higher ids =
-    // lower cta) therefore run no later than its owner, and at any moment only
-    // ~1/(waves+1) of the CTAs are in the bandwidth-heavy balanced region.
-    const int64_t hi = s.bal.first_id + s.bal.count;
-    const int64_t u = hi - 1 - cta;
-    const int64_t waves = (s.dp_tiles + P - 1) / P;
-    const int64_t slot = u >= s.bal.first_id ? cta * (waves + 1) / P : -1;
-    int64_t j = 0;
-    for (int64_t i = cta; i < s.dp_tiles; i += P, ++j) {
-      if (j == slot) run_unit(s, u, f);
-      run_unit(s, s.dp_id0 + raster_tile(s, i, raster_rows), f);
-    }
-    if (slot >= j) run_unit(s, u, f);
-  } else if (s.dp_id0 > s.bal.first_id && order == kDpFirst) {  // TwoTileSkDp, DP wave(s) first
-    dp_phase();
-    desc_phase(s.bal.first_id, s.bal.first_id + s.bal.count);
-  } else {  // StreamK, DpOneTileSk, TwoTileSkDp with the SK region first (Fig. 4c)
-    desc_phase(s.bal.first_id, s.bal.first_id + s.bal.count);
-    dp_phase();
-  }
+  SegmentIter sit(s, cta, P, lane, raster_rows, order);
+  int64_t u, tile, lb, le;
+  while (sit.next(s, &u, &tile, &lb, &le)) f(u, tile, lb, le);
 }
 
 #pragma nv_exec_check_disable
