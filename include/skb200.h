@@ -226,6 +226,12 @@ sk_status sk_timeline_size(const sk_gemm_desc* desc, int64_t* records, int64_t* 
  * *ok = 0.  die_of_sm may be NULL; at most max_sms entries are written. */
 sk_status sk_device_topology(int device, int32_t* die_of_sm, int32_t max_sms, int32_t* sms,
                              int32_t* ok);
+/* The persistent sequence CTA (pair) `cta` of a `num_ctas`-CTA launch of
+ * `desc` walks -- producer, MMA issuer and epilogue all follow it: records of
+ * {unit, tile, local_begin, local_end} (executor.hpp:149-185 segments), at
+ * most max_records written, *count = the sequence length.  Host-side. */
+sk_status sk_persistent_order(const sk_gemm_desc* desc, int64_t num_ctas, int64_t cta,
+                              int64_t* out, int64_t max_records, int64_t* count);
 /* Stream-ordered, asynchronous.  Does not synchronise. */
 sk_status sk_gemm(const sk_gemm_desc* desc, void* workspace, size_t workspace_bytes,
                   void* stream);

@@ -112,6 +112,8 @@ _SIGS = {
     "sk_timeline_size": (C.c_int, [_P(sk_gemm_desc), _P(C.c_int64), _P(C.c_int64)]),
     "sk_gemm": (C.c_int, [_P(sk_gemm_desc), C.c_void_p, C.c_size_t, C.c_void_p]),
     "sk_device_topology": (C.c_int, [C.c_int, C.c_void_p, C.c_int32, _P(C.c_int32), _P(C.c_int32)]),
+    "sk_persistent_order": (C.c_int, [_P(sk_gemm_desc), C.c_int64, C.c_int64, C.c_void_p, C.c_int64,
+                                      _P(C.c_int64)]),
     "sk_execute": (C.c_int, [_P(sk_problem), _P(sk_blocking), C.c_int, C.c_int64, C.c_int, C.c_int,
                              C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32]),
     "sk_execute_ranges": (C.c_int, [_P(sk_problem), _P(sk_blocking), C.c_void_p, C.c_int64, C.c_int,
@@ -575,6 +577,31 @@ def device_topology(device: int = 0) -> Optional[np.ndarray]:
     _check(lib().sk_device_topology(device, die.ctypes.data_as(C.c_void_p), 256, C.byref(sms),
                                     C.byref(ok)), "device_topology")
     return die[:sms.value].copy() if ok.value else None
+
+
+def persistent_order(a: WorkAssignment, num_ctas: int, ab_type: DType = DType.BFloat16,
+                     variant: Variant = Variant.TwoSM) -> List[np.ndarray]:
+    """Per persistent CTA (pair), the [n][4] int64 records {unit, tile,
+    local_begin, local_end} its producer / MMA issuer / epilogue walk in a
+    `num_ctas`-CTA launch (host-side, sk_persistent_order)."""
+    d = sk_gemm_desc()
+    d.problem, d.blocking = a.problem._c(), a.blocking._c()
+    d.strategy, d.param = int(a.strategy), a.param
+    table = _explicit_table(a) if a.param == 0 else None
+    if table is not None:
+        d.strategy, d.ranges, d.num_ranges = SK_EXPLICIT, table.ctypes.data, table.shape[0]
+    d.ab_type, d.variant = int(ab_type), int(variant)
+    d.lda, d.ldb, d.ldc = a.problem.k, a.problem.n, a.problem.n
+    out = []
+    for cta in range(num_ctas):
+        n = C.c_int64()
+        _check(lib().sk_persistent_order(C.byref(d), num_ctas, cta, None, 0, C.byref(n)),
+               "persistent_order")
+        rec = np.zeros((max(n.value, 1), 4), np.int64)
+        _check(lib().sk_persistent_order(C.byref(d), num_ctas, cta, rec.ctypes.data_as(C.c_void_p),
+                                         n.value, C.byref(n)), "persistent_order")
+        out.append(rec[:n.value])
+    return out
 
 
 def _host_type(arr: np.ndarray) -> DType:

@@ -445,6 +445,18 @@ int64_t raster_rows_for(const sk_gemm_desc* d) {
   return rows;
 }
 
+// Grouped tile ids (see gemm_impl): G = the raster height, after which the
+// data-parallel raster is the identity.
+void apply_tile_group(Kernel kern, bool explicit_table, bool pipelined, Schedule* s, int64_t* raster) {
+  if (pipelined || explicit_table || kern == Kernel::F64) return;
+  int64_t group = *raster;
+  if (const char* e = getenv("SKB200_TILE_GROUP")) group = std::max(1, atoi(e));
+  if (group > 1) {
+    s->tile_group = group;
+    *raster = 1;  // the id order already is the raster
+  }
+}
+
 // TwoTileSkDp phase order: the FP64 kernel runs the SK region first (its fixup
 // epilogues then overlap the DP waves: 33.6 -> 34.3 TFLOP/s at 8192^3); the
 // tcgen05 kernel keeps the DP waves first (SK-first measured 1.5 % slower;
@@ -684,6 +696,29 @@ sk_status sk_device_topology(int device, int32_t* die_of_sm, int32_t max_sms, in
   return SK_OK;
 }
 
+sk_status sk_persistent_order(const sk_gemm_desc* d, int64_t num_ctas, int64_t cta, int64_t* out,
+                              int64_t max_records, int64_t* count) {
+  Kernel kern;
+  Schedule s;
+  sk_status st = check_desc(d, &kern, &s);
+  if (st) return st;
+  if (num_ctas < 1 || cta < 0 || cta >= num_ctas || !count || (max_records > 0 && !out))
+    return fail(SK_EINVAL, "persistent_order: bad grid / cta / output");
+  int64_t raster = raster_rows_for(d);
+  apply_tile_group(kern, s.strategy == kExplicit, false, &s, &raster);
+  SegmentIter it(s, cta, num_ctas, default_lane(s, cta, num_ctas), raster, phase_order_for(kern));
+  int64_t n = 0, u, tile, lb, le;
+  while (it.next(s, &u, &tile, &lb, &le)) {
+    if (n < max_records) {
+      int64_t* r = out + 4 * n;
+      r[0] = u, r[1] = tile, r[2] = lb, r[3] = le;
+    }
+    ++n;
+  }
+  *count = n;
+  return SK_OK;
+}
+
 sk_status sk_gemm(const sk_gemm_desc* d, void* ws, size_t ws_bytes, void* stream) {
   return gemm_impl(d, ws, ws_bytes, static_cast<cudaStream_t>(stream), nullptr, nullptr);
 }
@@ -751,6 +786,7 @@ sk_status gemm_impl(const sk_gemm_desc* d, void* ws, size_t ws_bytes, cudaStream
   // kept near 32 MB so they stay L2-resident while B streams through; measured
   // best at 8192^3: 16 rows (1-SM), 8 rows (2-SM) (profiles/r01/raster_rows.txt).
   P.raster_rows = raster > 0 ? raster : raster_rows_for(d);
+  apply_tile_group(kern, xp, a_ready != nullptr, &P.s, &P.raster_rows);
   // Grouped tile ids (Schedule::tile_rc): the same G-row groups now also
   // decide which block of C each tile id denotes, so a hybrid's trailing
   // Stream-K region is a compact 8 x 17 block at 8192^3 instead of a
@@ -761,14 +797,6 @@ sk_status gemm_impl(const sk_gemm_desc* d, void* ws, size_t ws_bytes, cudaStream
   // zero is observable (the reference's row-major id).  The DMMA kernel keeps
   // its raster (it is compute-bound, insensitive to L2 placement).
   // SKB200_TILE_GROUP=1 restores the reference's row-major tile ids.
-  if (!a_ready && !xp && kern != Kernel::F64) {
-    int64_t group = P.raster_rows;
-    if (const char* e = getenv("SKB200_TILE_GROUP")) group = std::max(1, atoi(e));
-    if (group > 1) {
-      P.s.tile_group = group;
-      P.raster_rows = 1;  // the id order already is the raster
-    }
-  }
   // L2 eviction priorities {A loads, B loads, C stores}: 0 normal, 1 first, 2 last.
   // A panels are re-read across a raster group's waves (keep), B panels stream
   // through a wave and C is written once (evict first); measured +4 % at 8192^3
