@@ -232,6 +232,10 @@ sk_status sk_device_topology(int device, int32_t* die_of_sm, int32_t max_sms, in
  * most max_records written, *count = the sequence length.  Host-side. */
 sk_status sk_persistent_order(const sk_gemm_desc* desc, int64_t num_ctas, int64_t cta,
                               int64_t* out, int64_t max_records, int64_t* count);
+/* The block of C (tile row, tile column) that tile id `tile` denotes in a
+ * launch of `desc` (not pipelined): row-major like executor.hpp:69-70 for
+ * explicit tables and the FP64 kernel, grouped rows otherwise. */
+sk_status sk_tile_block(const sk_gemm_desc* desc, int64_t tile, int64_t* tile_row, int64_t* tile_col);
 /* Stream-ordered, asynchronous.  Does not synchronise. */
 sk_status sk_gemm(const sk_gemm_desc* desc, void* workspace, size_t workspace_bytes,
                   void* stream);

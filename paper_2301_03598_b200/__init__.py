@@ -114,6 +114,7 @@ _SIGS = {
     "sk_device_topology": (C.c_int, [C.c_int, C.c_void_p, C.c_int32, _P(C.c_int32), _P(C.c_int32)]),
     "sk_persistent_order": (C.c_int, [_P(sk_gemm_desc), C.c_int64, C.c_int64, C.c_void_p, C.c_int64,
                                       _P(C.c_int64)]),
+    "sk_tile_block": (C.c_int, [_P(sk_gemm_desc), C.c_int64, _P(C.c_int64), _P(C.c_int64)]),
     "sk_execute": (C.c_int, [_P(sk_problem), _P(sk_blocking), C.c_int, C.c_int64, C.c_int, C.c_int,
                              C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32]),
     "sk_execute_ranges": (C.c_int, [_P(sk_problem), _P(sk_blocking), C.c_void_p, C.c_int64, C.c_int,
@@ -579,11 +580,7 @@ def device_topology(device: int = 0) -> Optional[np.ndarray]:
     return die[:sms.value].copy() if ok.value else None
 
 
-def persistent_order(a: WorkAssignment, num_ctas: int, ab_type: DType = DType.BFloat16,
-                     variant: Variant = Variant.TwoSM) -> List[np.ndarray]:
-    """Per persistent CTA (pair), the [n][4] int64 records {unit, tile,
-    local_begin, local_end} its producer / MMA issuer / epilogue walk in a
-    `num_ctas`-CTA launch (host-side, sk_persistent_order)."""
+def _launch_desc(a: WorkAssignment, ab_type: DType, variant: Variant):
     d = sk_gemm_desc()
     d.problem, d.blocking = a.problem._c(), a.blocking._c()
     d.strategy, d.param = int(a.strategy), a.param
@@ -592,6 +589,15 @@ def persistent_order(a: WorkAssignment, num_ctas: int, ab_type: DType = DType.BF
         d.strategy, d.ranges, d.num_ranges = SK_EXPLICIT, table.ctypes.data, table.shape[0]
     d.ab_type, d.variant = int(ab_type), int(variant)
     d.lda, d.ldb, d.ldc = a.problem.k, a.problem.n, a.problem.n
+    return d, table
+
+
+def persistent_order(a: WorkAssignment, num_ctas: int, ab_type: DType = DType.BFloat16,
+                     variant: Variant = Variant.TwoSM) -> List[np.ndarray]:
+    """Per persistent CTA (pair), the [n][4] int64 records {unit, tile,
+    local_begin, local_end} its producer / MMA issuer / epilogue walk in a
+    `num_ctas`-CTA launch (host-side, sk_persistent_order)."""
+    d, _table = _launch_desc(a, ab_type, variant)
     out = []
     for cta in range(num_ctas):
         n = C.c_int64()
@@ -601,6 +607,19 @@ def persistent_order(a: WorkAssignment, num_ctas: int, ab_type: DType = DType.BF
         _check(lib().sk_persistent_order(C.byref(d), num_ctas, cta, rec.ctypes.data_as(C.c_void_p),
                                          n.value, C.byref(n)), "persistent_order")
         out.append(rec[:n.value])
+    return out
+
+
+def tile_blocks(a: WorkAssignment, ab_type: DType = DType.BFloat16,
+                variant: Variant = Variant.TwoSM) -> np.ndarray:
+    """[t][2] (tile row, tile column) of C each tile id denotes on the device
+    (sk_tile_block)."""
+    d, _table = _launch_desc(a, ab_type, variant)
+    out = np.zeros((a.grid.total_tiles, 2), np.int64)
+    r, c = C.c_int64(), C.c_int64()
+    for t in range(a.grid.total_tiles):
+        _check(lib().sk_tile_block(C.byref(d), t, C.byref(r), C.byref(c)), "tile_block")
+        out[t] = (r.value, c.value)
     return out
 
 

@@ -719,6 +719,19 @@ sk_status sk_persistent_order(const sk_gemm_desc* d, int64_t num_ctas, int64_t c
   return SK_OK;
 }
 
+sk_status sk_tile_block(const sk_gemm_desc* d, int64_t tile, int64_t* tile_row, int64_t* tile_col) {
+  Kernel kern;
+  Schedule s;
+  sk_status st = check_desc(d, &kern, &s);
+  if (st) return st;
+  if (!tile_row || !tile_col) return fail(SK_EINVAL, "null output");
+  if (tile < 0 || tile >= s.total_tiles) return fail(SK_ERANGE, "tile %lld out of range", (long long)tile);
+  int64_t raster = raster_rows_for(d);
+  apply_tile_group(kern, s.strategy == kExplicit, false, &s, &raster);
+  s.tile_rc(tile, tile_row, tile_col);
+  return SK_OK;
+}
+
 sk_status sk_gemm(const sk_gemm_desc* d, void* ws, size_t ws_bytes, void* stream) {
   return gemm_impl(d, ws, ws_bytes, static_cast<cudaStream_t>(stream), nullptr, nullptr);
 }

@@ -14,6 +14,8 @@ decomposition (decompose.cpp) -- CPU only, no device needed:
 """
 import itertools
 
+import numpy as np
+
 import pytest
 
 
@@ -104,3 +106,27 @@ def _dp_unit(sk, a, u):
     if a.strategy == sk.Strategy.DpOneTileSk:  # DP ids [0, w*p), SK ids after
         return u < w * p
     return u >= p  # TwoTileSkDp: SK ids [0, p), DP ids [p, p + d)
+
+
+@pytest.mark.parametrize("shape,blk", CASES + [((8192, 8192, 64), (256, 256, 64)),
+                                               ((4000, 300, 777), (128, 256, 64))])
+def test_tile_blocks_bijection(sk, shape, blk, monkeypatch):
+    """Grouped tile ids (Schedule::tile_rc) denote every block of C exactly once;
+    SKB200_TILE_GROUP=1 and the FP64 kernel keep the reference's row-major map
+    (executor.hpp:69-70)."""
+    problem = sk.GemmProblem(*shape)
+    b = sk.BlockingFactors(*blk)
+    variant = sk.Variant.TwoSM if blk[0] == 256 else sk.Variant.OneSM
+    a = sk.stream_k(problem, b, 74)
+    tm, tn = a.grid.tiles_m, a.grid.tiles_n
+    row_major = np.array([(t // tn, t % tn) for t in range(tm * tn)])
+    blocks = sk.tile_blocks(a, variant=variant)
+    assert sorted(map(tuple, blocks.tolist())) == sorted(map(tuple, row_major.tolist()))
+    monkeypatch.setenv("SKB200_TILE_GROUP", "1")
+    assert np.array_equal(sk.tile_blocks(a, variant=variant), row_major)
+    monkeypatch.delenv("SKB200_TILE_GROUP")
+    b64 = sk.kernel_blocking(sk.DType.Float64)
+    a64 = sk.stream_k(problem, b64, 296)
+    t64 = a64.grid.tiles_n
+    want = np.array([(t // t64, t % t64) for t in range(a64.grid.total_tiles)])
+    assert np.array_equal(sk.tile_blocks(a64, sk.DType.Float64, sk.Variant.Auto), want)
