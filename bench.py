@@ -364,6 +364,15 @@ def main():
         sweep = {"shapes": "%s (%d)" % (label, len(shapes)), "policy": "stream_k:auto (cost model)",
                  "geomean_sk_vs_dp": summ["geomean_speedup"], "min": summ["min"],
                  "max": summ["max"], "regress_gt_5pct": summ["regress_gt_5pct"]}
+        if args.dtype != "fp64":
+            # bandwidth-bound skinny shapes (below the ridge): HBM GB/s vs the measured peak
+            hbm = load_peaks()[1]
+            srows = sw.run(sw.SKINNY[:2] + sw.SKINNY[4:6], ["data_parallel", "stream_k:auto"], variant,
+                           args.dtype)
+            sweep["skinny_hbm"] = [
+                {"shape": [r["m"], r["n"], r["k"]], "strategy": r["strategy"], "g": r["g"],
+                 "gbps": round(r["gbps"], 1), "frac_of_hbm_peak": round(r["gbps"] / hbm, 3)}
+                for r in srows]
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:

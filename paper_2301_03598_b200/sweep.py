@@ -30,16 +30,22 @@ import numpy as np
 
 import paper_2301_03598_b200 as sk
 
-SCHEMA = "# schema=sk_b200/1"
+SCHEMA = "# schema=sk_b200/2"  # /2: + gbps (algorithmic A + B + C bytes / time)
 COLUMNS = ["m", "n", "k", "tiles_m", "tiles_n", "t", "iters_per_tile", "strategy", "param", "g",
            "schedule", "variant", "dtype",
-           "copies", "l2_cold", "time_us", "tflops"]
+           "copies", "l2_cold", "time_us", "tflops", "gbps"]
 L2_BYTES = 126 * 1024 * 1024
 
 CONFIG3 = [
     (1024, 1024, 32768), (1280, 3840, 4096), (1280, 3840, 8192), (1024, 4864, 4096),
     (2560, 3840, 4096), (1024, 1024, 8192), (512, 512, 65536), (3072, 3072, 3072),
     (2304, 2304, 8192), (1280, 7680, 4096), (4096, 4096, 4096), (8192, 8192, 8192),
+]
+# Bandwidth-bound skinny shapes (128 x 8192 x 8192 has ~122
+# FLOP/B, below the B200 ridge of ~250): reported in HBM GB/s as well.
+SKINNY = [
+    (128, 8192, 8192), (256, 8192, 8192), (128, 16384, 8192), (8192, 128, 8192),
+    (64, 8192, 16384), (128, 4096, 16384), (512, 8192, 4096), (256, 16384, 2048),
 ]
 # BASELINE config 4: FP64 squares 1024..8192 with the paper's 64x64x16 tile,
 # plus shapes whose 64x64 tile count sits just above a multiple of 296 CTAs.
@@ -132,6 +138,13 @@ class ShapeTimer:
         return best
 
 
+def algorithmic_bytes(m, n, k, dtype):
+    """Compulsory traffic: A and B read once, C written once (beta = 0)."""
+    es = 8 if dtype == "fp64" else 2
+    cs = 8 if dtype == "fp64" else 4
+    return es * (m * k + k * n) + cs * m * n
+
+
 def run(shapes, names, variant, dtype, rank=0, world=1, log_every=0, params=None):
     import torch
 
@@ -160,7 +173,8 @@ def run(shapes, names, variant, dtype, rank=0, world=1, log_every=0, params=None
                          "variant": "dmma" if dtype == "fp64" else (
                              "2sm" if variant == sk.Variant.TwoSM else "1sm"),
                          "dtype": dtype, "copies": timer.copies, "l2_cold": int(timer.cold),
-                         "time_us": t, "tflops": 2.0 * m * n * k / (t * 1e-6) / 1e12})
+                         "time_us": t, "tflops": 2.0 * m * n * k / (t * 1e-6) / 1e12,
+                         "gbps": algorithmic_bytes(m, n, k, dtype) / (t * 1e-6) / 1e9})
         del timer
         if log_every and (idx // world) % log_every == 0:
             print(f"[rank {rank}] {idx}/{len(shapes)} {m}x{n}x{k}", file=sys.stderr, flush=True)
@@ -181,6 +195,12 @@ def summarise(rows, baseline="data_parallel", tol=0.05):
             out[name] = {"geomean_speedup": float(np.exp(np.mean(np.log(sp)))),
                          "min": float(min(sp)), "max": float(max(sp)),
                          "regress_gt_5pct": int(sum(s < 1 - tol for s in sp))}
+    gb = {}
+    for r in rows:
+        if "gbps" in r:
+            gb.setdefault(r["strategy"], []).append(r["gbps"])
+    if gb:
+        out["median_gbps"] = {k: float(np.median(v)) for k, v in sorted(gb.items())}
     return out
 
 
@@ -210,7 +230,7 @@ def write_csv(path, rows):
 
 def main(argv=None):
     ap = argparse.ArgumentParser()
-    ap.add_argument("--shapes", default="config3", choices=["config3", "config4", "corpus"])
+    ap.add_argument("--shapes", default="config3", choices=["config3", "config4", "corpus", "skinny"])
     ap.add_argument("--count", type=int, default=32824)
     ap.add_argument("--offset", type=int, default=0)
     ap.add_argument("--lo", type=int, default=128)
@@ -234,6 +254,8 @@ def main(argv=None):
         shapes = CONFIG3
     elif args.shapes == "config4":
         shapes = CONFIG4
+    elif args.shapes == "skinny":
+        shapes = SKINNY
     else:
         c = sk.corpus(args.seed, args.offset + args.count, args.lo, args.hi)[args.offset:]
         shapes = [tuple(int(x) for x in r[:3]) for r in c]
