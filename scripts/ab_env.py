@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--k", type=int, default=8192)
     ap.add_argument("--dtype", default="bf16")
     ap.add_argument("--g", type=int, default=74, help="stream_k grid / hybrid p")
+    ap.add_argument("--variant", default="2sm", choices=["1sm", "2sm"])
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--rounds", type=int, default=4)
@@ -44,7 +45,8 @@ def main():
     A = (torch.rand(m, pad(k, 8), device="cuda") * 2 - 1).to(tdt)[:, :k]
     B = (torch.rand(k, pad(n, 8), device="cuda") * 2 - 1).to(tdt)[:, :n]
     C = torch.empty(m, pad(n, 4), device="cuda", dtype=torch.float32)[:, :n]
-    blk = sk.kernel_blocking(ab, sk.Variant.TwoSM)
+    V = sk.Variant.TwoSM if args.variant == "2sm" else sk.Variant.OneSM
+    blk = sk.kernel_blocking(ab, V)
     prob = sk.GemmProblem(m, n, k)
     if args.strategy == "data_parallel":
         a = sk.data_parallel(prob, blk)
@@ -52,7 +54,7 @@ def main():
         a = sk.stream_k(prob, blk, args.g)
     else:
         a = sk.hybrid(prob, blk, args.g, sk.HybridVariant.TwoTileSkDp)
-    g = sk.Gemm(a, ab, sk.Variant.TwoSM)
+    g = sk.Gemm(a, ab, V)
     stream = torch.cuda.current_stream()
     flops = 2.0 * m * n * k
     arms = [dict(kv.split("=", 1) for kv in s.split(",")) for s in args.set]
