@@ -210,7 +210,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         // unrelated k offsets by Stream-K units: separate L2 priorities.
         const bool sk_unit = s.strategy == kFixedSplit || s.bal.contains_id(u);
         const uint64_t pol_b = sk_unit ? pol_b_sk : pol_b_dp;
-        if (P.a_ready) wait_flag(P, P.a_ready + tr);  // row block of A in HBM
+        if (P.a_ready) {  // row block of A (and column panel of B) in HBM
+          wait_flag(P, P.a_ready + tr);
+          if (P.b_ready) wait_flag(P, P.b_ready + tc / P.pipe_w);
+        }
         // k order of a balanced unit's segments (P.k_align): see k_block_of.
         int64_t rot = -1;
         if (P.k_align && sk_unit && s.strategy != kFixedSplit) {
@@ -489,7 +492,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             ptx::tma_store_wait_all<0>();
             ptx::fence_proxy_async_global();
             __threadfence_system();
-            atomicAdd(P.c_done + tr, 1);
+            atomicAdd(P.c_done + SK_CDONE_INDEX(P, tr, tc), 1);
           }
           __syncwarp();
         }

@@ -99,7 +99,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
         s.tile_rc(tile, &tr, &tc);
         const int32_t m0 = static_cast<int32_t>(tr * BM);
         const int32_t n0 = static_cast<int32_t>(tc * BN);
-        if (P.a_ready) wait_flag(P, P.a_ready + tr);  // row block of A in HBM
+        if (P.a_ready) {  // row block of A (and column panel of B) in HBM
+          wait_flag(P, P.a_ready + tr);
+          if (P.b_ready) wait_flag(P, P.b_ready + tc / P.pipe_w);
+        }
         for (int64_t kb = lb; kb < le; ++kb) {
           ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
           ptx::mbar_expect_tx(&full_bar[stage], STAGE_BYTES);
@@ -248,7 +251,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
     if (P.c_done) {  // the tile is in HBM: count it for copy-out
       __threadfence_system();
       ptx::named_bar_sync(1, 128);
-      if (tid == 0) atomicAdd(P.c_done + tr, 1);
+      if (tid == 0) atomicAdd(P.c_done + SK_CDONE_INDEX(P, tr, tc), 1);
     }
     if (ev) {
       if (npeer == 0) ev[kEvWaitEnd] = ev[kEvMacEnd];

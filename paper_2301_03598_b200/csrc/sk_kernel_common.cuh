@@ -38,6 +38,9 @@ struct WorkspaceLayout {
   }
 };
 
+// c_done counter of tile (tr, tc) under the pipelining block geometry.
+#define SK_CDONE_INDEX(P, tr, tc) ((tr) / (P).pipe_g * (P).pipe_np + (tc) / (P).pipe_w)
+
 // Error word bits.
 enum : int { kErrDoubleSignal = 1, kErrWatchdog = 1 << 16, kErrTopology = 1 << 17 };
 
@@ -67,6 +70,12 @@ struct KernelParams {
   // stream can start on the row before the kernel ends.
   const int* a_ready;
   int* c_done;
+  // Tile-block pipelining (16-bit kernels): B also arrives by panels of pipe_w
+  // tile columns (b_ready[panel], NULL = B already complete), and c_done counts
+  // per block of pipe_g tile rows x pipe_w tile columns (pipe_np panels per row
+  // of blocks); the per-row scheme is pipe_g = 1, pipe_w = tiles_n.
+  const int* b_ready;
+  int32_t pipe_g, pipe_w, pipe_np;
   int32_t k_align;  // balanced units: aligned k order (k_block_of), 0 = ascending
   int32_t l2_policy[4];  // L2 eviction priority for A loads, B loads (data-parallel
                          // units), C stores, B loads (Stream-K / fixed-split units):

@@ -19,6 +19,7 @@
 #include <mutex>
 #include <string>
 #include <unordered_map>
+#include <tuple>
 #include <vector>
 
 #include "../../include/skb200.h"
@@ -431,8 +432,16 @@ sk_status check_desc(const sk_gemm_desc* d, Kernel* kern, Schedule* s) {
 }  // namespace
 
 namespace {
+// Transfer-pipelining state of a launch (sk_execute with pinned host buffers).
+struct PipeFlags {
+  const int* a_ready = nullptr;  // [tiles_m]
+  const int* b_ready = nullptr;  // [panels] or NULL (B complete before launch)
+  int* c_done = nullptr;         // [blocks]
+  int g = 1, w = 1, np = 1;      // c_done block = g tile rows x w tile cols; np panels
+  int64_t raster = 1;            // data-parallel raster height
+};
 sk_status gemm_impl(const sk_gemm_desc* d, void* ws, size_t ws_bytes, cudaStream_t strm,
-                    const int* a_ready, int* c_done, int64_t raster = 0);
+                    const PipeFlags* pipe = nullptr);
 
 // Raster group height: the group's A panels (rows x BLK_M x k elements) are
 // kept near 32 MB so they stay L2-resident while B streams through; measured
@@ -733,14 +742,17 @@ sk_status sk_tile_block(const sk_gemm_desc* d, int64_t tile, int64_t* tile_row, 
 }
 
 sk_status sk_gemm(const sk_gemm_desc* d, void* ws, size_t ws_bytes, void* stream) {
-  return gemm_impl(d, ws, ws_bytes, static_cast<cudaStream_t>(stream), nullptr, nullptr);
+  return gemm_impl(d, ws, ws_bytes, static_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"
 
 namespace {
 sk_status gemm_impl(const sk_gemm_desc* d, void* ws, size_t ws_bytes, cudaStream_t strm,
-                    const int* a_ready, int* c_done, int64_t raster) {
+                    const PipeFlags* pipe) {
+  const int* a_ready = pipe ? pipe->a_ready : nullptr;
+  int* c_done = pipe ? pipe->c_done : nullptr;
+  const int64_t raster = pipe ? pipe->raster : 0;
   Kernel kern;
   Schedule s;
   sk_status st = check_desc(d, &kern, &s);
@@ -791,6 +803,10 @@ sk_status gemm_impl(const sk_gemm_desc* d, void* ws, size_t ws_bytes, cudaStream
   P.trace = d->trace;
   P.a_ready = a_ready;
   P.c_done = c_done;
+  P.b_ready = pipe ? pipe->b_ready : nullptr;
+  P.pipe_g = pipe ? pipe->g : 1;
+  P.pipe_w = pipe ? pipe->w : static_cast<int32_t>(s.tiles_n);
+  P.pipe_np = pipe ? pipe->np : 1;
   P.cta_clocks = reinterpret_cast<long long*>(d->cta_clocks);
   P.events = reinterpret_cast<long long*>(d->events);
   P.seg_stride = d->events ? max_segments_per_unit(s) : 1;
@@ -996,61 +1012,87 @@ bool is_pinned(const void* p) {
   return a.type == cudaMemoryTypeHost;
 }
 
-// Transfer pipelining for sk_execute (pinned host buffers, no conversion): the
-// kernel starts once B is in HBM; A arrives row block by row block on a copy
-// stream (the producer waits on a_ready[row]) and every finished tile row of C
-// leaves on a second copy stream (cuStreamWaitValue32 on c_done[row]) while the
-// kernel still runs, so H2D, compute and D2H overlap.  The schedule is the
-// caller's: only copy order follows it.  Rows are copied in, and waited for,
-// in the order the persistent traversal first needs / last stores them.
+// Transfer pipelining for sk_execute (pinned host buffers, no conversion): A
+// arrives by tile rows and B by panels of W tile columns on a copy stream, each
+// followed by a flag the producer waits on (a_ready[row], b_ready[panel]), in
+// the order the persistent traversal first needs them; every finished block of
+// C (G tile rows x W tile columns, counted by c_done[block]) leaves on a second
+// copy stream (cuStreamWaitValue32) while the kernel still runs.  G is the data-
+// parallel raster height, so a raster group's first wave needs only its G rows
+// of A and the first few panels of B, and C starts leaving after the first
+// group's columns instead of after all of B (profiles/r01d/pipeline_blocks.txt).
+// The FP64 kernel keeps whole-B-first, row blocks of C (G = 1, W = tiles_n).
+// The schedule is the caller's: only copy order follows it.
 sk_status execute_pipelined(ExecCache& X, sk_gemm_desc& d, size_t ws_bytes, const void* A,
                             const void* B, void* C, size_t esz, size_t csz, bool zero_c) {
   Kernel kern;
   Schedule s;
   sk_status st = check_desc(&d, &kern, &s);
   if (st) return st;
-  const int64_t m = d.problem.m, n = d.problem.n, k = d.problem.k, bm = d.blocking.blk_m;
-  const int64_t rows = s.tiles_m;
+  const int64_t m = d.problem.m, n = d.problem.n, k = d.problem.k;
+  const int64_t bm = d.blocking.blk_m, bn = d.blocking.blk_n;
+  const int64_t rows = s.tiles_m, cols = s.tiles_n;
+  const bool f64 = kern == Kernel::F64;
+  PipeFlags pf;
+  // Block geometry: G = 1 / W = all columns is the whole-B-first, row-block
+  // scheme (kept for FP64); the tcgen05 kernels use 8 x 8 tile blocks, 2 %
+  // faster at 8192^3 (8.39-8.48 vs 8.60-8.66 ms; profiles/r01d/pipeline_blocks.txt):
+  // the call is bound by bidirectional PCIe, not by when C starts to leave.
+  int64_t G = f64 ? 1 : 8, W = f64 ? cols : 8;
+  if (!f64) {
+    if (const char* e = getenv("SKB200_PIPE_G")) G = std::max(1, atoi(e));
+    if (const char* e = getenv("SKB200_PIPE_W")) W = std::max(1, atoi(e));
+  }
+  pf.raster = std::min<int64_t>(rows, G);
+  pf.g = static_cast<int>(pf.raster);
+  pf.w = static_cast<int>(std::min<int64_t>(cols, W));
+  pf.np = static_cast<int>((cols + pf.w - 1) / pf.w);
+  const int64_t groups = (rows + pf.g - 1) / pf.g, blocks = groups * pf.np;
   // stores per tile: one per epilogue warp of each CTA of the pair (tcgen05), one (DMMA)
-  const uint32_t incr = kern == Kernel::F64 ? 1u
-                        : static_cast<uint32_t>(kernel_ranks(kern) * f16_epilogue_warps());
-  std::vector<uint32_t> target(static_cast<size_t>(rows), 0);
-  std::vector<int64_t> first(static_cast<size_t>(rows), INT64_MAX), last(static_cast<size_t>(rows), -1);
+  const uint32_t incr = f64 ? 1u : static_cast<uint32_t>(kernel_ranks(kern) * f16_epilogue_warps());
+  std::vector<uint32_t> target(static_cast<size_t>(blocks), 0);
+  std::vector<int64_t> firstA(static_cast<size_t>(rows), INT64_MAX), firstB(static_cast<size_t>(pf.np), INT64_MAX);
+  std::vector<int64_t> lastC(static_cast<size_t>(blocks), -1);
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t P = std::max<int64_t>(1, std::min<int64_t>(std::max<int64_t>(s.grid_size, 1),
-                                                           kern == Kernel::F64 ? 2 * sms : sms / kernel_ranks(kern)));
-  // Row-major data-parallel order: whole rows of C finish early and stream out
-  // while the rest computes (the kernel is a small part of the transfer-bound call).
-  const int64_t raster = 1;
+                                                           f64 ? 2 * sms : sms / kernel_ranks(kern)));
   const int order = phase_order_for(kern);
   for (int64_t cta = 0; cta < P; ++cta) {
     int64_t t = 0;
-    for_each_segment(s, cta, P, raster, [&](int64_t, int64_t tile, int64_t lb, int64_t le) {
-      const size_t r = static_cast<size_t>(tile / s.tiles_n);
-      first[r] = std::min(first[r], t);
+    for_each_segment(s, cta, P, pf.raster, [&](int64_t, int64_t tile, int64_t lb, int64_t le) {
+      int64_t tr, tc;
+      s.tile_rc(tile, &tr, &tc);
+      const size_t blk = static_cast<size_t>(tr / pf.g * pf.np + tc / pf.w);
+      firstA[static_cast<size_t>(tr)] = std::min(firstA[static_cast<size_t>(tr)], t);
+      firstB[static_cast<size_t>(tc / pf.w)] = std::min(firstB[static_cast<size_t>(tc / pf.w)], t);
       t += le - lb;
       if (lb == 0) {
-        last[r] = std::max(last[r], t);
-        target[r] += incr;
+        lastC[blk] = std::max(lastC[blk], t);
+        target[blk] += incr;
       }
     }, order);
   }
-  std::vector<int64_t> in_order(static_cast<size_t>(rows)), out_order;
-  for (int64_t r = 0; r < rows; ++r) in_order[static_cast<size_t>(r)] = r;
-  out_order = in_order;
-  std::stable_sort(in_order.begin(), in_order.end(), [&](int64_t x, int64_t y) {
-    return first[static_cast<size_t>(x)] < first[static_cast<size_t>(y)];
-  });
+  // copy-in items: (first need, kind 0 = A row / 1 = B panel, index), B first on ties
+  std::vector<std::tuple<int64_t, int, int64_t>> items;
+  for (int64_t r = 0; r < rows; ++r) items.emplace_back(firstA[static_cast<size_t>(r)], 0, r);
+  for (int64_t q = 0; q < pf.np; ++q) items.emplace_back(firstB[static_cast<size_t>(q)], -1, q);
+  std::stable_sort(items.begin(), items.end());
+  std::vector<int64_t> out_order(static_cast<size_t>(blocks));
+  for (int64_t b = 0; b < blocks; ++b) out_order[static_cast<size_t>(b)] = b;
   std::stable_sort(out_order.begin(), out_order.end(), [&](int64_t x, int64_t y) {
-    return last[static_cast<size_t>(x)] < last[static_cast<size_t>(y)];
+    return lastC[static_cast<size_t>(x)] < lastC[static_cast<size_t>(y)];
   });
 
-  st = X.ensure(5, sizeof(int) * static_cast<size_t>(2 * rows));
+  st = X.ensure(5, sizeof(int) * static_cast<size_t>(rows + pf.np + blocks));
   if (st) return st;
   int* a_ready = static_cast<int*>(X.buf[5]);
-  int* c_done = a_ready + rows;
+  int* b_ready = a_ready + rows;
+  int* c_done = b_ready + pf.np;
+  pf.a_ready = a_ready;
+  pf.b_ready = b_ready;
+  pf.c_done = c_done;
   if (!X.s_in) {
     SK_CUDA(cudaStreamCreateWithFlags(&X.s_in, cudaStreamNonBlocking));
     SK_CUDA(cudaStreamCreateWithFlags(&X.s_out, cudaStreamNonBlocking));
@@ -1058,65 +1100,68 @@ sk_status execute_pipelined(ExecCache& X, sk_gemm_desc& d, size_t ws_bytes, cons
     SK_CUDA(cudaEventCreateWithFlags(&X.ev_flags, cudaEventDisableTiming));
   }
   cudaStream_t sm = X.stream, si = X.s_in, so = X.s_out;
-  // copy-in: flags down, all of B, then A row blocks (each followed by its flag)
-  SK_CUDA(cudaMemsetAsync(a_ready, 0, sizeof(int) * static_cast<size_t>(2 * rows), si));
-  SK_CUDA(copy_rows(X.buf[1], d.ldb * esz, B, n * esz, n * esz, k, cudaMemcpyHostToDevice, si));
+  // flags down before the kernel and the copy-out waits see them
+  SK_CUDA(cudaMemsetAsync(a_ready, 0, sizeof(int) * static_cast<size_t>(rows + pf.np + blocks), si));
   SK_CUDA(cudaEventRecord(X.ev_in, si));
   SK_CUDA(cudaStreamWaitEvent(sm, X.ev_in, 0));
-  SK_CUDA(cudaEventRecord(X.ev_flags, sm));  // orders c_done's reset before copy-out waits
+  SK_CUDA(cudaStreamWaitEvent(so, X.ev_in, 0));
   d.A = X.buf[0];
   d.B = X.buf[1];
   d.C = X.buf[2];
   if (zero_c) SK_CUDA(cudaMemsetAsync(X.buf[2], 0, static_cast<size_t>(m * d.ldc) * csz, sm));
-  st = gemm_impl(&d, X.buf[3], ws_bytes, sm, a_ready, c_done, raster);
+  st = gemm_impl(&d, X.buf[3], ws_bytes, sm, &pf);
   if (st) return st;
+  // a stream memory op, not a memset kernel: nothing may need an SM the
+  // persistent GEMM is holding
+  auto raise = [&](const int* flag) -> sk_status {
+    const CUresult cr = write_value32()(reinterpret_cast<CUstream>(si), reinterpret_cast<CUdeviceptr>(flag),
+                                        1, CU_STREAM_WRITE_VALUE_DEFAULT);
+    return cr == CUDA_SUCCESS ? SK_OK : fail(SK_ECUDA, "cuStreamWriteValue32 failed (%d)", int(cr));
+  };
   const uint8_t* Ah = static_cast<const uint8_t*>(A);
+  const uint8_t* Bh = static_cast<const uint8_t*>(B);
   uint8_t* Ad = static_cast<uint8_t*>(X.buf[0]);
-  // Consecutive row blocks travel as one copy of up to ~16 MB (per-copy gaps
+  uint8_t* Bd = static_cast<uint8_t*>(X.buf[1]);
+  // Consecutive A row blocks travel as one copy of up to ~16 MB (per-copy gaps
   // cost more than the later first row, profiles/r01/pipeline.txt).
   const int64_t max_rows = std::max<int64_t>(1, (int64_t(16) << 20) / std::max<int64_t>(1, bm * k * static_cast<int64_t>(esz)));
-  for (size_t i = 0; i < in_order.size();) {
+  for (size_t i = 0; i < items.size();) {
+    const int kind = std::get<1>(items[i]);
+    const int64_t idx = std::get<2>(items[i]);
+    if (kind != 0) {  // B panel: W tile columns x all k rows (2-D copy)
+      const int64_t c0 = idx * pf.w * bn, nc = std::min<int64_t>(c0 + pf.w * bn, n) - c0;
+      SK_CUDA(copy_rows(Bd + static_cast<size_t>(c0) * esz, d.ldb * esz, Bh + static_cast<size_t>(c0) * esz,
+                        n * esz, nc * esz, k, cudaMemcpyHostToDevice, si));
+      if ((st = raise(b_ready + idx))) return st;
+      ++i;
+      continue;
+    }
     size_t j = i + 1;
-    while (j < in_order.size() && in_order[j] == in_order[j - 1] + 1 &&
-           static_cast<int64_t>(j - i) < max_rows)
+    while (j < items.size() && std::get<1>(items[j]) == 0 &&
+           std::get<2>(items[j]) == std::get<2>(items[j - 1]) + 1 && static_cast<int64_t>(j - i) < max_rows)
       ++j;
-    const int64_t r0 = in_order[i] * bm, nr = std::min(in_order[j - 1] * bm + bm, m) - r0;
+    const int64_t r0 = idx * bm, nr = std::min(std::get<2>(items[j - 1]) * bm + bm, m) - r0;
     SK_CUDA(copy_rows(Ad + static_cast<size_t>(r0 * d.lda) * esz, d.lda * esz,
                       Ah + static_cast<size_t>(r0 * k) * esz, k * esz, k * esz, nr,
                       cudaMemcpyHostToDevice, si));
-    // a stream memory op, not a memset kernel: nothing may need an SM the
-    // persistent GEMM is holding
-    for (size_t q = i; q < j; ++q) {
-      const CUresult cr = write_value32()(reinterpret_cast<CUstream>(si),
-                                          reinterpret_cast<CUdeviceptr>(a_ready + in_order[q]), 1,
-                                          CU_STREAM_WRITE_VALUE_DEFAULT);
-      if (cr != CUDA_SUCCESS) return fail(SK_ECUDA, "cuStreamWriteValue32 failed (%d)", int(cr));
-    }
+    for (size_t q = i; q < j; ++q)
+      if ((st = raise(a_ready + std::get<2>(items[q])))) return st;
     i = j;
   }
-  // copy-out: each tile row once all of its stores have landed
-  SK_CUDA(cudaStreamWaitEvent(so, X.ev_flags, 0));
+  // copy-out: each block of C once all of its stores have landed
   uint8_t* Ch = static_cast<uint8_t*>(C);
   const uint8_t* Cd = static_cast<const uint8_t*>(X.buf[2]);
   PFN_waitValue32 wv = wait_value32();
-  const int64_t max_out = std::max<int64_t>(1, (int64_t(16) << 20) / std::max<int64_t>(1, bm * n * static_cast<int64_t>(csz)));
-  for (size_t i = 0; i < out_order.size();) {
-    size_t j = i + 1;
-    while (j < out_order.size() && out_order[j] == out_order[j - 1] + 1 &&
-           static_cast<int64_t>(j - i) < max_out)
-      ++j;
-    for (size_t q = i; q < j; ++q) {
-      const int64_t r = out_order[q];
-      if (!target[static_cast<size_t>(r)]) continue;  // nothing stores it (explicit tables)
-      const CUresult cr = wv(reinterpret_cast<CUstream>(so), reinterpret_cast<CUdeviceptr>(c_done + r),
-                             target[static_cast<size_t>(r)], CU_STREAM_WAIT_VALUE_GEQ);
-      if (cr != CUDA_SUCCESS) return fail(SK_ECUDA, "cuStreamWaitValue32 failed (%d)", int(cr));
-    }
-    const int64_t r0 = out_order[i] * bm, nr = std::min(out_order[j - 1] * bm + bm, m) - r0;
-    SK_CUDA(copy_rows(Ch + static_cast<size_t>(r0 * n) * csz, n * csz,
-                      Cd + static_cast<size_t>(r0 * d.ldc) * csz, d.ldc * csz, n * csz, nr,
+  for (int64_t b : out_order) {
+    if (!target[static_cast<size_t>(b)]) continue;  // nothing stores it (explicit tables)
+    const CUresult cr = wv(reinterpret_cast<CUstream>(so), reinterpret_cast<CUdeviceptr>(c_done + b),
+                           target[static_cast<size_t>(b)], CU_STREAM_WAIT_VALUE_GEQ);
+    if (cr != CUDA_SUCCESS) return fail(SK_ECUDA, "cuStreamWaitValue32 failed (%d)", int(cr));
+    const int64_t r0 = (b / pf.np) * pf.g * bm, nr = std::min(r0 + pf.g * bm, m) - r0;
+    const int64_t c0 = (b % pf.np) * pf.w * bn, nc = std::min(c0 + pf.w * bn, n) - c0;
+    SK_CUDA(copy_rows(Ch + static_cast<size_t>(r0 * n + c0) * csz, n * csz,
+                      Cd + static_cast<size_t>(r0 * d.ldc + c0) * csz, d.ldc * csz, nc * csz, nr,
                       cudaMemcpyDeviceToHost, so));
-    i = j;
   }
   SK_CUDA(cudaStreamSynchronize(si));
   SK_CUDA(cudaStreamSynchronize(so));

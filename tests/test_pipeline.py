@@ -1,7 +1,8 @@
 """sk_execute with pinned host buffers overlaps H2D, compute and D2H (A arrives
-row block by row block behind flags the producer waits on; finished C rows leave
-on a copy stream while the kernel runs).  The schedule and the arithmetic are
-unchanged, so C must be bit-identical to the serial path and to the oracle."""
+by tile rows and B by column panels behind flags the producer waits on; finished
+blocks of C leave on a copy stream while the kernel runs).  The schedule is
+unchanged, so on integer-valued data C must be bit-identical to the serial path
+and to the oracle."""
 import os
 
 import numpy as np
@@ -32,7 +33,8 @@ def run(sk, a, A, B, compute, variant, pipeline, out):
 
 
 @pytest.mark.parametrize("var", ["1sm", "2sm", "fp64"])
-@pytest.mark.parametrize("shape", [(1000, 1000, 520), (2048, 768, 1024), (777, 1300, 333)])
+@pytest.mark.parametrize("shape", [(1000, 1000, 520), (2048, 768, 1024), (777, 1300, 333),
+                                   (2100, 2600, 700)])
 def test_pipelined_execute_bit_identical(sk, port, torch_cuda, var, shape):
     torch = torch_cuda
     m, n, k = shape
