@@ -349,8 +349,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         __syncwarp();
         const float* os = slab(own_base + fidx(owner));
+        const int c_end = m0 + static_cast<int32_t>(q * 32) >= s.m
+                              ? c_lo
+                              : imin(c_lo + EPI_COLS / 32, 2 * ceil_div(s.n - n0, 64));
 #pragma unroll 1
-        for (int c = c_lo + idx; c < c_lo + EPI_COLS / 32; c += ncon) {
+        for (int c = c_lo + idx; c < c_end; c += ncon) {
           float4 a[8];
 #pragma unroll
           for (int j = 0; j < 8; ++j) a[j] = ptx::ld_cg_f4(slab_ptr(const_cast<float*>(os), c, j, row));
@@ -435,8 +438,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       float* my_slab = publish ? slab(my_idx) : nullptr;
       // 64 columns (two 32-column chunks) per step: one tcgen05.ld.x64, 16 float4
       // of peer slab in flight per thread, two 32x32 TMA-store boxes.
+      // Only chunks that hold part of C: this warp's 32 rows and the 64-column
+      // steps left of n (ragged edges, skinny m or n); every contributor of the
+      // tile skips the same (rows, chunk) pairs, so publish and fold stay matched.
+      const int c_end = (orphan || m0 + static_cast<int32_t>(q * 32) >= s.m)
+                            ? c_lo
+                            : imin(c_lo + EPI_COLS / 32, 2 * ceil_div(s.n - n0, 64));
 #pragma unroll 1
-      for (int c = c_lo; c < (orphan ? c_lo : c_lo + EPI_COLS / 32); c += 2) {
+      for (int c = c_lo; c < c_end; c += 2) {
         float v[64];
         ptx::tmem_ld64(tsrc + c * 32, v);
         if (publish) {
