@@ -57,7 +57,16 @@ def main():
     g = sk.Gemm(a, ab, V)
     stream = torch.cuda.current_stream()
     flops = 2.0 * m * n * k
-    arms = [dict(kv.split("=", 1) for kv in s.split(",")) for s in args.set]
+    def parse_arm(spec):  # VAR=VALUE pairs separated by commas; values may contain commas
+        pairs = []
+        for tok in spec.split(","):
+            if "=" in tok or not pairs:
+                pairs.append(tok)
+            else:
+                pairs[-1] += "," + tok
+        return dict(kv.split("=", 1) for kv in pairs)
+
+    arms = [parse_arm(s) for s in args.set]
     res = [[] for _ in arms]
     ref = None
     for _ in range(args.rounds):
