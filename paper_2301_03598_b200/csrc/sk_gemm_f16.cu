@@ -39,7 +39,15 @@ namespace f16 {
 
 constexpr int ROWS = 128;  // rows per CTA (= TMEM lanes)
 constexpr int BN = 256;    // tile columns (MMA N)
-constexpr int BK = 64;
+constexpr int BK = 64;  // k-depth of one Stream-K iteration (the blocking factor)
+// k-depth of one smem stage: 64 (one iteration) or 32 (half-depth stages: twice
+// as many, released after 2 MMAs instead of 4, A in 64-B swizzle).
+#ifndef SKB200_STAGE_K
+#define SKB200_STAGE_K 64
+#endif
+constexpr int BKS = SKB200_STAGE_K;
+constexpr int SUB = BK / BKS;
+static_assert(BKS == 64 || BKS == 32, "stage k-depth 64 or 32");
 constexpr int UMMA_K = 16;
 // Epilogue warps: 4 (one per TMEM lane quarter) or 8 (two per quarter, each
 // draining half of the 256 accumulator columns -- twice the loads/stores in
@@ -62,13 +70,13 @@ constexpr int EPI_BYTES = EPI_WARPS * EPI_BUFS * EPI_BUF_BYTES;
 constexpr int NUM_THREADS = 64 + 32 * EPI_WARPS;  // 320 (192 with 4 epilogue warps)
 constexpr int TMEM_COLS = 512;                    // 2 x 256-col accumulators
 constexpr int SLAB_ELEMS = ROWS * BN;             // fp32 partial per CTA rank
-constexpr int B_BOX_BYTES = 64 * BK * 2;          // 64 k-rows x 64 cols
+constexpr int B_BOX_BYTES = 64 * BKS * 2;         // BKS k-rows x 64 cols
 
 template <int CG>
 struct Cfg {
   static constexpr int B_COLS = BN / CG;                    // B columns held per CTA
-  static constexpr int A_STAGE = ROWS * BK * 2;             // 16 KB
-  static constexpr int B_STAGE = B_COLS * BK * 2;           // 32 KB (1-SM) / 16 KB (2-SM)
+  static constexpr int A_STAGE = ROWS * BKS * 2;            // 16 KB (BKS = 64)
+  static constexpr int B_STAGE = B_COLS * BKS * 2;          // 32 KB (1-SM) / 16 KB (2-SM)
   static constexpr int STAGE = A_STAGE + B_STAGE;
 #ifndef SKB200_STAGES_1SM
 #define SKB200_STAGES_1SM 4
@@ -76,7 +84,7 @@ struct Cfg {
 #ifndef SKB200_STAGES_2SM
 #define SKB200_STAGES_2SM 6
 #endif
-  static constexpr int STAGES = CG == 1 ? SKB200_STAGES_1SM : SKB200_STAGES_2SM;
+  static constexpr int STAGES = (CG == 1 ? SKB200_STAGES_1SM : SKB200_STAGES_2SM) * SUB;
   static constexpr int a_off = 0;
   static constexpr int b_off = a_off + STAGES * A_STAGE;
   static constexpr int epi_off = b_off + STAGES * B_STAGE;
@@ -223,8 +231,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         for (int64_t i = lb; i < le; ++i) {
           const int64_t kb = rot < 0 ? i : k_block_of(s.ipt, lb, le, rot, i - lb);
+          for (int h = 0; h < SUB; ++h) {
           ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
-          const int32_t k0 = static_cast<int32_t>(kb * BK);
+          const int32_t k0 = static_cast<int32_t>(kb * BK + h * BKS);
           uint8_t* a_dst = sA + stage * K::A_STAGE;
           uint8_t* b_dst = sB + stage * K::B_STAGE;
           if constexpr (CG == 1) {
@@ -246,6 +255,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             stage = 0;
             phase ^= 1;
           }
+          }
         }
       }, P.sk_first);
     }
@@ -261,18 +271,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (long long* ev = event_slot(P, u, tile)) ev[kEvMacStart] = ptx::globaltimer();
         const uint32_t d_tmem = tmem_base + acc * BN;
         for (int64_t kb = lb; kb < le; ++kb) {
+          for (int h = 0; h < SUB; ++h) {
           ptx::mbar_wait(&full_bar[stage], phase);
           ptx::tc_fence_after();
           const uint32_t a0 = ptx::smem_u32(sA + stage * K::A_STAGE);
           const uint32_t b0 = ptx::smem_u32(sB + stage * K::B_STAGE);
 #pragma unroll
-          for (int kk = 0; kk < BK / UMMA_K; ++kk) {
-            // A: K-major SW128, +32 B per 16-element k step; SBO = 8 rows x 128 B.
-            const uint64_t ad = ptx::make_sdesc_sw128(a0 + kk * 32, 16, 1024);
+          for (int kk = 0; kk < BKS / UMMA_K; ++kk) {
+            // A: K-major, swizzle = row bytes (128 B at BKS 64, 64 B at 32), +32 B per
+            // 16-element k step; SBO = 8 rows x row bytes.
+            const uint64_t ad = BKS == 64 ? ptx::make_sdesc_sw128(a0 + kk * 32, 16, 1024)
+                                          : ptx::make_sdesc_sw64(a0 + kk * 32, 16, 512);
             // B: MN-major SW128, +16 k-rows x 128 B per k step; LBO = next 64-col box,
             // SBO = 8 k-rows x 128 B.
             const uint64_t bd = ptx::make_sdesc_sw128(b0 + kk * 2048, B_BOX_BYTES, 1024);
-            ptx::umma_f16<CG>(d_tmem, ad, bd, P.idesc, (kb > lb || kk > 0) ? 1u : 0u);
+            ptx::umma_f16<CG>(d_tmem, ad, bd, P.idesc, (kb > lb || h > 0 || kk > 0) ? 1u : 0u);
           }
           // Free the smem slot(s) once these MMAs have read them.
           if constexpr (CG == 1) ptx::umma_commit(&empty_bar[stage]);
@@ -280,6 +293,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (++stage == K::STAGES) {
             stage = 0;
             phase ^= 1;
+          }
           }
         }
         // Accumulator ready for the epilogue warps (of both CTAs for CG = 2).
@@ -568,6 +582,7 @@ uint32_t make_idesc_f16(bool bf16, int M, int N) {
 }
 
 size_t f16_slab_bytes() { return sizeof(float) * f16::SLAB_ELEMS; }
+int f16_stage_k() { return f16::BKS; }
 int f16_epilogue_warps() { return f16::EPI_WARPS; }
 
 template <int CG>

@@ -30,6 +30,7 @@ namespace skb200 {
 // sk_gemm_f16.cu
 uint32_t make_idesc_f16(bool bf16, int M, int N);
 size_t f16_slab_bytes();
+int f16_stage_k();
 int f16_epilogue_warps();
 cudaError_t launch_f16(int cg, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
                        const KernelParams& p, int grid, cudaStream_t stream);
@@ -876,10 +877,11 @@ sk_status gemm_impl(const sk_gemm_desc* d, void* ws, size_t ws_bytes, cudaStream
     const CUtensorMapDataType dt = d->ab_type == SK_BFLOAT16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
                                                              : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
     CUtensorMap ta, tb, tc;
-    st = make_tmap(&ta, dt, 2, d->A, d->problem.m, d->problem.k, d->lda, 64, 128,
-                   CU_TENSOR_MAP_SWIZZLE_128B);
+    const int bks = f16_stage_k();  // smem stage k-depth (A rows of bks elements)
+    st = make_tmap(&ta, dt, 2, d->A, d->problem.m, d->problem.k, d->lda, static_cast<uint32_t>(bks), 128,
+                   bks == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B);
     if (st) return st;
-    st = make_tmap(&tb, dt, 2, d->B, d->problem.k, d->problem.n, d->ldb, 64, 64,
+    st = make_tmap(&tb, dt, 2, d->B, d->problem.k, d->problem.n, d->ldb, 64, static_cast<uint32_t>(bks),
                    CU_TENSOR_MAP_SWIZZLE_128B);
     if (st) return st;
     st = make_tmap(&tc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, d->C, d->problem.m, d->problem.n,
