@@ -111,8 +111,12 @@ class ClockSampler:
             time.sleep(0.001)
 
     def __enter__(self):
+        import sys
         import threading
 
+        # the poller must get the GIL between the launch loop's Python steps
+        self._switch = sys.getswitchinterval()
+        sys.setswitchinterval(0.0002)
         try:
             import pynvml as nv
 
@@ -127,9 +131,12 @@ class ClockSampler:
         return self
 
     def __exit__(self, *exc):
+        import sys
+
         self.stop = True
         if self.thread:
             self.thread.join()
+        sys.setswitchinterval(self._switch)
 
     def summary(self):
         if not self.samples:
