@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
           }
         }
-      }, P.sk_first);
+      }, P.sk_first, P.dp_perm);
     }
     __syncwarp();
   } else if (warp == 1) {
@@ -301,7 +301,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         else ptx::umma_commit_mc(&tfull_bar[acc], 0x3);
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
-      }, P.sk_first);
+      }, P.sk_first, P.dp_perm);
     }
     __syncwarp();
   } else {
@@ -556,7 +556,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           npend = 0;
         }
       }
-    }, P.sk_first);
+    }, P.sk_first, P.dp_perm);
     if (lane == 0) ptx::tma_store_wait_all<0>();
     __syncwarp();
   }

@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
             phase ^= 1;
           }
         }
-      }, P.sk_first);
+      }, P.sk_first, P.dp_perm);
     }
     return;
   }
@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
       if (npeer == 0) ev[kEvWaitEnd] = ev[kEvMacEnd];
       ev[kEvDone] = ptx::globaltimer();
     }
-  }, P.sk_first);
+  }, P.sk_first, P.dp_perm);
   stamp_clock(P, 1);
 #endif
 }

@@ -76,6 +76,7 @@ struct KernelParams {
   // of blocks); the per-row scheme is pipe_g = 1, pipe_w = tiles_n.
   const int* b_ready;
   int32_t pipe_g, pipe_w, pipe_np;
+  const int32_t* dp_perm;  // pipelined: data-parallel slot -> tile order (NULL = raster)
   int32_t k_align;  // balanced units: aligned k order (k_block_of), 0 = ascending
   int32_t l2_policy[4];  // L2 eviction priority for A loads, B loads (data-parallel
                          // units), C stores, B loads (Stream-K / fixed-split units):
@@ -170,10 +171,11 @@ struct SegmentIter {
   bool fresh = true;          // phase not started yet
   int64_t ins_unit = -1, ins_slot = -1, j = 0;  // kInterleaved: unit, slot, DP tiles so far
   int64_t u = 0, it = 0, e = 0;
+  const int32_t* perm = nullptr;  // optional DP slot -> tile permutation (pipelined execute)
 
   SK_HD SegmentIter(const Schedule& s, int64_t cta_, int64_t P_, const DpLane& lane_,
-                    int64_t raster_, int order)
-      : cta(cta_), P(P_), raster(raster_), lane(lane_) {
+                    int64_t raster_, int order, const int32_t* perm_ = nullptr)
+      : cta(cta_), P(P_), raster(raster_), lane(lane_), perm(perm_) {
     const bool two_tile_dp_first = s.dp_id0 > s.bal.first_id;
     if (s.strategy == kFixedSplit || s.strategy == kExplicit) {
       kind0 = kDesc, nph = 1, lo = 0, hi = s.grid_size;
@@ -211,7 +213,7 @@ struct SegmentIter {
         fresh = false;
         if (i < lane.end) {
           ++j;
-          return load(s, s.dp_id0 + raster_tile(s, i, raster));
+          return load(s, s.dp_id0 + (perm ? perm[i] : raster_tile(s, i, raster)));
         }
         if (ins_unit >= 0) {  // its slot lies past this CTA's last DP tile
           const int64_t uu = ins_unit;
@@ -255,8 +257,9 @@ struct SegmentIter {
 #pragma nv_exec_check_disable
 template <class F>
 SK_HD void for_each_segment(const Schedule& s, int64_t cta, int64_t P, const DpLane& lane,
-                            int64_t raster_rows, F&& f, int order = kDpFirst) {
-  SegmentIter sit(s, cta, P, lane, raster_rows, order);
+                            int64_t raster_rows, F&& f, int order = kDpFirst,
+                            const int32_t* perm = nullptr) {
+  SegmentIter sit(s, cta, P, lane, raster_rows, order, perm);
   int64_t u, tile, lb, le;
   while (sit.next(s, &u, &tile, &lb, &le)) f(u, tile, lb, le);
 }
@@ -264,8 +267,8 @@ SK_HD void for_each_segment(const Schedule& s, int64_t cta, int64_t P, const DpL
 #pragma nv_exec_check_disable
 template <class F>
 SK_HD void for_each_segment(const Schedule& s, int64_t cta, int64_t P, int64_t raster_rows, F&& f,
-                            int order = kDpFirst) {
-  for_each_segment(s, cta, P, default_lane(s, cta, P), raster_rows, static_cast<F&&>(f), order);
+                            int order = kDpFirst, const int32_t* perm = nullptr) {
+  for_each_segment(s, cta, P, default_lane(s, cta, P), raster_rows, static_cast<F&&>(f), order, perm);
 }
 
 // k-block order inside a balanced unit's tile segment (the set of k-blocks is

@@ -440,6 +440,7 @@ struct PipeFlags {
   int* c_done = nullptr;         // [blocks]
   int g = 1, w = 1, np = 1;      // c_done block = g tile rows x w tile cols; np panels
   int64_t raster = 1;            // data-parallel raster height
+  const int32_t* perm = nullptr; // data-parallel slot -> tile order (device), or NULL
 };
 sk_status gemm_impl(const sk_gemm_desc* d, void* ws, size_t ws_bytes, cudaStream_t strm,
                     const PipeFlags* pipe = nullptr);
@@ -805,6 +806,7 @@ sk_status gemm_impl(const sk_gemm_desc* d, void* ws, size_t ws_bytes, cudaStream
   P.a_ready = a_ready;
   P.c_done = c_done;
   P.b_ready = pipe ? pipe->b_ready : nullptr;
+  P.dp_perm = pipe ? pipe->perm : nullptr;
   P.pipe_g = pipe ? pipe->g : 1;
   P.pipe_w = pipe ? pipe->w : static_cast<int32_t>(s.tiles_n);
   P.pipe_np = pipe ? pipe->np : 1;
@@ -1061,6 +1063,26 @@ sk_status execute_pipelined(ExecCache& X, sk_gemm_desc& d, size_t ws_bytes, cons
   const int64_t P = std::max<int64_t>(1, std::min<int64_t>(std::max<int64_t>(s.grid_size, 1),
                                                            f64 ? 2 * sms : sms / kernel_ranks(kern)));
   const int order = phase_order_for(kern);
+  // Data-parallel tiles in "growing square" block order: block (group, panel)
+  // shells of max(group, panel), each new B panel's blocks, then each new A
+  // group's, so every 32-MB input that lands completes more blocks of C and the
+  // copy-out never starves (profiles/r01d/pipeline_blocks.txt).  Row-major ids.
+  std::vector<int32_t> perm;
+  if (!f64) {
+    const int64_t R = groups, Cp = pf.np;
+    std::vector<std::pair<int64_t, int64_t>> border;
+    for (int64_t sh = 0; sh < std::max(R, Cp); ++sh) {
+      if (sh < Cp)
+        for (int64_t gi = 0; gi < std::min(sh, R); ++gi) border.emplace_back(gi, sh);
+      if (sh < R)
+        for (int64_t pj = 0; pj <= std::min(sh, Cp - 1); ++pj) border.emplace_back(sh, pj);
+    }
+    for (auto& bp : border)
+      for (int64_t tc = bp.second * pf.w; tc < std::min(cols, (bp.second + 1) * pf.w); ++tc)
+        for (int64_t tr = bp.first * pf.g; tr < std::min(rows, (bp.first + 1) * pf.g); ++tr)
+          if (tr * cols + tc < s.dp_tiles) perm.push_back(static_cast<int32_t>(tr * cols + tc));
+  }
+  const int32_t* hperm = perm.empty() ? nullptr : perm.data();
   for (int64_t cta = 0; cta < P; ++cta) {
     int64_t t = 0;
     for_each_segment(s, cta, P, pf.raster, [&](int64_t, int64_t tile, int64_t lb, int64_t le) {
@@ -1074,27 +1096,45 @@ sk_status execute_pipelined(ExecCache& X, sk_gemm_desc& d, size_t ws_bytes, cons
         lastC[blk] = std::max(lastC[blk], t);
         target[blk] += incr;
       }
-    }, order);
+    }, order, hperm);
   }
-  // copy-in items: (first need, kind 0 = A row / 1 = B panel, index), B first on ties
-  std::vector<std::tuple<int64_t, int, int64_t>> items;
-  for (int64_t r = 0; r < rows; ++r) items.emplace_back(firstA[static_cast<size_t>(r)], 0, r);
-  for (int64_t q = 0; q < pf.np; ++q) items.emplace_back(firstB[static_cast<size_t>(q)], -1, q);
-  std::stable_sort(items.begin(), items.end());
   std::vector<int64_t> out_order(static_cast<size_t>(blocks));
   for (int64_t b = 0; b < blocks; ++b) out_order[static_cast<size_t>(b)] = b;
   std::stable_sort(out_order.begin(), out_order.end(), [&](int64_t x, int64_t y) {
     return lastC[static_cast<size_t>(x)] < lastC[static_cast<size_t>(y)];
   });
+  // Copy-in order: by the first C block (in copy-out order) an item feeds, then
+  // by first need -- the copy-out is the long pole, so the inputs of the first
+  // block to leave come first (profiles/r01d/pipeline_blocks.txt).
+  std::vector<int64_t> pos(static_cast<size_t>(blocks));
+  for (int64_t i = 0; i < blocks; ++i) pos[static_cast<size_t>(out_order[static_cast<size_t>(i)])] = i;
+  std::vector<int64_t> feedA(static_cast<size_t>(rows), INT64_MAX), feedB(static_cast<size_t>(pf.np), INT64_MAX);
+  for (int64_t tr = 0; tr < rows; ++tr)
+    for (int64_t tc = 0; tc < cols; ++tc) {
+      const int64_t p = pos[static_cast<size_t>(tr / pf.g * pf.np + tc / pf.w)];
+      feedA[static_cast<size_t>(tr)] = std::min(feedA[static_cast<size_t>(tr)], p);
+      feedB[static_cast<size_t>(tc / pf.w)] = std::min(feedB[static_cast<size_t>(tc / pf.w)], p);
+    }
+  // items: (first block fed, first need, kind 0 = A row / -1 = B panel, index)
+  std::vector<std::tuple<int64_t, int64_t, int, int64_t>> items4;
+  for (int64_t r = 0; r < rows; ++r)
+    items4.emplace_back(feedA[static_cast<size_t>(r)], firstA[static_cast<size_t>(r)], 0, r);
+  for (int64_t q = 0; q < pf.np; ++q)
+    items4.emplace_back(feedB[static_cast<size_t>(q)], firstB[static_cast<size_t>(q)], -1, q);
+  std::stable_sort(items4.begin(), items4.end());
+  std::vector<std::tuple<int64_t, int, int64_t>> items;
+  for (auto& it4 : items4) items.emplace_back(std::get<1>(it4), std::get<2>(it4), std::get<3>(it4));
 
-  st = X.ensure(5, sizeof(int) * static_cast<size_t>(rows + pf.np + blocks));
+  st = X.ensure(5, sizeof(int) * static_cast<size_t>(rows + pf.np + blocks + perm.size()));
   if (st) return st;
   int* a_ready = static_cast<int*>(X.buf[5]);
   int* b_ready = a_ready + rows;
   int* c_done = b_ready + pf.np;
+  int32_t* dperm = c_done + blocks;
   pf.a_ready = a_ready;
   pf.b_ready = b_ready;
   pf.c_done = c_done;
+  pf.perm = perm.empty() ? nullptr : dperm;
   if (!X.s_in) {
     SK_CUDA(cudaStreamCreateWithFlags(&X.s_in, cudaStreamNonBlocking));
     SK_CUDA(cudaStreamCreateWithFlags(&X.s_out, cudaStreamNonBlocking));
@@ -1104,6 +1144,8 @@ sk_status execute_pipelined(ExecCache& X, sk_gemm_desc& d, size_t ws_bytes, cons
   cudaStream_t sm = X.stream, si = X.s_in, so = X.s_out;
   // flags down before the kernel and the copy-out waits see them
   SK_CUDA(cudaMemsetAsync(a_ready, 0, sizeof(int) * static_cast<size_t>(rows + pf.np + blocks), si));
+  if (!perm.empty())  // pageable source: staged by the runtime before the call returns
+    SK_CUDA(cudaMemcpyAsync(dperm, perm.data(), sizeof(int32_t) * perm.size(), cudaMemcpyHostToDevice, si));
   SK_CUDA(cudaEventRecord(X.ev_in, si));
   SK_CUDA(cudaStreamWaitEvent(sm, X.ev_in, 0));
   SK_CUDA(cudaStreamWaitEvent(so, X.ev_in, 0));
@@ -1111,8 +1153,23 @@ sk_status execute_pipelined(ExecCache& X, sk_gemm_desc& d, size_t ws_bytes, cons
   d.B = X.buf[1];
   d.C = X.buf[2];
   if (zero_c) SK_CUDA(cudaMemsetAsync(X.buf[2], 0, static_cast<size_t>(m * d.ldc) * csz, sm));
+  // SKB200_PIPE_TRACE=1: event after every copy and the kernel, printed to
+  // stderr in ms from the call's start (profiles/r01d/pipeline_blocks.txt)
+  const char* tr_env = getenv("SKB200_PIPE_TRACE");
+  const bool trace = tr_env && atoi(tr_env) != 0;
+  std::vector<std::pair<std::string, cudaEvent_t>> tev;
+  auto mark = [&](const std::string& what, cudaStream_t q) {
+    if (!trace) return;
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) == cudaSuccess) {
+      cudaEventRecord(e, q);
+      tev.emplace_back(what, e);
+    }
+  };
+  mark("start", si);
   st = gemm_impl(&d, X.buf[3], ws_bytes, sm, &pf);
   if (st) return st;
+  mark("kernel_end", sm);
   // a stream memory op, not a memset kernel: nothing may need an SM the
   // persistent GEMM is holding
   auto raise = [&](const int* flag) -> sk_status {
@@ -1135,6 +1192,7 @@ sk_status execute_pipelined(ExecCache& X, sk_gemm_desc& d, size_t ws_bytes, cons
       SK_CUDA(copy_rows(Bd + static_cast<size_t>(c0) * esz, d.ldb * esz, Bh + static_cast<size_t>(c0) * esz,
                         n * esz, nc * esz, k, cudaMemcpyHostToDevice, si));
       if ((st = raise(b_ready + idx))) return st;
+      mark("B_panel_" + std::to_string(idx), si);
       ++i;
       continue;
     }
@@ -1148,6 +1206,7 @@ sk_status execute_pipelined(ExecCache& X, sk_gemm_desc& d, size_t ws_bytes, cons
                       cudaMemcpyHostToDevice, si));
     for (size_t q = i; q < j; ++q)
       if ((st = raise(a_ready + std::get<2>(items[q])))) return st;
+    mark("A_rows_" + std::to_string(idx) + "-" + std::to_string(std::get<2>(items[j - 1])), si);
     i = j;
   }
   // copy-out: each block of C once all of its stores have landed
@@ -1164,9 +1223,19 @@ sk_status execute_pipelined(ExecCache& X, sk_gemm_desc& d, size_t ws_bytes, cons
     SK_CUDA(copy_rows(Ch + static_cast<size_t>(r0 * n + c0) * csz, n * csz,
                       Cd + static_cast<size_t>(r0 * d.ldc + c0) * csz, d.ldc * csz, nc * csz, nr,
                       cudaMemcpyDeviceToHost, so));
+    mark("C_block_" + std::to_string(b), so);
   }
   SK_CUDA(cudaStreamSynchronize(si));
   SK_CUDA(cudaStreamSynchronize(so));
+  if (trace && !tev.empty()) {
+    cudaDeviceSynchronize();
+    for (auto& te : tev) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, tev[0].second, te.second);
+      fprintf(stderr, "[pipe] %8.3f ms %s\n", ms, te.first.c_str());
+    }
+    for (auto& te : tev) cudaEventDestroy(te.second);
+  }
   return sk_workspace_check(X.buf[3], sm);
 }
 
