@@ -26,6 +26,11 @@
 // Smem ring: STAGES k-blocks of A (rows x 64, K-major, 128B swizzle) and B
 // (64 x cols as 64x64 boxes, MN-major, 128B swizzle).  TMEM: two 256-column
 // fp32 accumulators, so one segment's epilogue overlaps the next mainloop.
+// All roles walk the same SegmentIter sequence (sk_kernel_common.cuh); tile ids
+// denote C blocks through Schedule::tile_rc (grouped rows).  Fixup: the owner
+// folds its peers (executor.hpp order), or -- schedules of >= 8 contributors per
+// tile, one unit per CTA -- every contributor publishes and folds a column
+// share (coop_fold).  Pieces of a tile outside C are skipped throughout.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
