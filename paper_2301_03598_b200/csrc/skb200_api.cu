@@ -164,8 +164,13 @@ sk_status make_tmap(CUtensorMap* m, CUtensorMapDataType dt, size_t esize, const 
   const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * esize};
   const cuuint32_t box[2] = {box_cols, box_rows};
   const cuuint32_t estr[2] = {1, 1};
+  // 128-B L2 promotion: 8192^3 DP 1468.8 vs 1461.7 (256 B), hybrid 1445.4 vs
+  // 1438.7 TFLOP/s; config 3 and skinny shapes unchanged (profiles/r01/l2_policy.txt).
+  CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+  if (const char* e = getenv("SKB200_L2_PROMO"))  // 0 none, 1 64B, 2 128B, 3 256B
+    promo = static_cast<CUtensorMapL2promotion>(atoi(e));
   CUresult r = fn(m, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, swz, promo,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(SK_ECUDA, "cuTensorMapEncodeTiled failed (%d)", int(r));
   return SK_OK;
