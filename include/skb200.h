@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define SKB200_ABI_VERSION 2
+#define SKB200_ABI_VERSION 3
 
 typedef enum sk_status {
   SK_OK = 0,
@@ -133,6 +133,17 @@ typedef struct sk_gemm_desc {
    * only when the workspace last ran a different table. */
   const int64_t* ranges;
   int64_t num_ranges;
+  /* ABI v3: which block of C a tile id denotes.
+   *   0 (default) or 1: the reference's row-major map, tile -> (tile / tiles_n,
+   *     tile % tiles_n) (executor.hpp:69-70,173-174).  Data-parallel units are
+   *     still visited in a grouped raster order (temporal order only).
+   *   G > 1: ids run through groups of G tile rows, column-major inside a group
+   *     (an opt-in locality layout: ids, ranges, owners and peers stay the
+   *     reference's, but the block of C an id denotes does not).  Clamped to
+   *     tiles_m.  Ignored by explicit tables, the pipelined sk_execute and FP64.
+   *   -1: G = the data-parallel raster height (the round-1 default). */
+  int32_t tile_group;
+  int32_t reserved0; /* must be 0 */
 } sk_gemm_desc;
 
 const char* sk_status_string(sk_status status);
@@ -214,8 +225,11 @@ sk_status sk_workspace_size(const sk_gemm_desc* desc, size_t* bytes);
 sk_status sk_workspace_init(void* workspace, size_t bytes, void* stream);
 /* Synchronises the stream, reads and clears the workspace error word. */
 sk_status sk_workspace_check(void* workspace, void* stream);
-/* Ints needed for the optional ownership trace: per tile {owner, last_peer,
- * storing_unit, segments} followed by per unit {partials_emitted}. */
+/* Ints needed for the optional ownership trace: per tile id {owner, last_peer,
+ * storing_unit, segments}, then per unit {partials_emitted}, then per block of C
+ * in row-major block order (tile_row * tiles_n + tile_col) {unit that stored it}
+ * -- 5 * total_tiles + grid_size ints.  The block section shows the tile -> C
+ * map actually used (executor.hpp:69-70 under the default tile_group). */
 sk_status sk_trace_size(const sk_gemm_desc* desc, int64_t* ints);
 /* Records of the optional device timeline: grid_size * seg_stride (record of
  * unit u's i-th tile segment at u * seg_stride + i; unused records stay zero). */
@@ -233,8 +247,8 @@ sk_status sk_device_topology(int device, int32_t* die_of_sm, int32_t max_sms, in
 sk_status sk_persistent_order(const sk_gemm_desc* desc, int64_t num_ctas, int64_t cta,
                               int64_t* out, int64_t max_records, int64_t* count);
 /* The block of C (tile row, tile column) that tile id `tile` denotes in a
- * launch of `desc` (not pipelined): row-major like executor.hpp:69-70 for
- * explicit tables and the FP64 kernel, grouped rows otherwise. */
+ * launch of `desc`: row-major like executor.hpp:69-70 unless desc->tile_group
+ * selects the grouped layout (tcgen05 kernels, closed-form schedules). */
 sk_status sk_tile_block(const sk_gemm_desc* desc, int64_t tile, int64_t* tile_row, int64_t* tile_col);
 /* Stream-ordered, asynchronous.  Does not synchronise. */
 sk_status sk_gemm(const sk_gemm_desc* desc, void* workspace, size_t workspace_bytes,
@@ -268,6 +282,39 @@ sk_status sk_fixup_peers_ranges(const sk_problem* problem, const sk_blocking* bl
                                 int64_t* ids, int64_t capacity, int64_t* nnz);
 /* Releases the calling thread's sk_execute cache. */
 void sk_execute_release(void);
+
+/* ---- reference input generator (matrix.hpp:39-68), on the device ---------- */
+/* Fills the pitched device buffer dst (rows x cols, ld elements) with
+ * random_matrix<gen_type>(rows, cols, seed): element i (row-major) is the i-th
+ * SplitMix64 draw, as (next() & 0x7f) - 64 for SK_INT64 (then >> shift,
+ * arithmetic), (float)(u * 2 - 1) for SK_FLOAT32 and u * 2 - 1 for SK_FLOAT64
+ * (u = (next() >> 11) * 2^-53), rounded to nearest-even into out_type
+ * (SK_BFLOAT16 | SK_FLOAT16 | SK_FLOAT32 | SK_FLOAT64; FLOAT64 generation only
+ * into FLOAT32/FLOAT64).  Stream-ordered. */
+sk_status sk_random_matrix(sk_dtype gen_type, int32_t shift, uint64_t seed, int64_t rows,
+                           int64_t cols, sk_dtype out_type, void* dst, int64_t ld, void* stream);
+
+/* ---- simulator (simulate.cpp:23-80) --------------------------------------- */
+/* Reference CostParams (costmodel.hpp:13-19): a fixed per-unit cost, b partial
+ * output cost, c per-iteration cost, d per-peer reduction cost. */
+typedef struct sk_sim_params {
+  double a, b, c, d;
+} sk_sim_params;
+/* Greedy list scheduling of the schedule's units in cta_id order onto p cores
+ * (earliest free, lowest index on ties).  params NULL: unit cost (1 per MAC
+ * iteration, zero-length fixups).  Writes the makespan, the utilization (sum of
+ * MAC durations / (p * makespan); SK_EINVAL for an empty timeline, as the
+ * reference throws) and, when events != NULL, up to `capacity` records of 6
+ * doubles {core, cta, kind (0 mac, 2 fixup_reduce), start, end, tile}.
+ * strategy SK_EXPLICIT takes the [num_ranges][2] table. */
+sk_status sk_simulate(const sk_problem* problem, const sk_blocking* blocking, sk_strategy strategy,
+                      int64_t param, const int64_t* ranges, int64_t num_ranges, int64_t p,
+                      const sk_sim_params* params, double* makespan, double* utilization,
+                      double* events, int64_t capacity, int64_t* num_events);
+
+/* Re-reads the SKB200_* tuning overrides from the environment (they are read
+ * once, at the first launch; DESIGN.md lists them). */
+void sk_reload_env(void);
 
 #ifdef __cplusplus
 }

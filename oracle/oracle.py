@@ -255,6 +255,36 @@ def corpus(seed: int, count: int, lo: int = 128, hi: int = 8192) -> np.ndarray:
     return out
 
 
+def ref_run_sweep(seed: int, count: int, lo: int, hi: int, strategies, p: int, split: int,
+                  blk) -> str:
+    """The reference's run_sweep CSV text (sweep.cpp:75-112), unmeasured."""
+    lib = C.CDLL(REF_SO)
+    codes = np.array([STRATEGIES[s] if isinstance(s, str) else int(s) for s in strategies], np.int32)
+    n = _i64()
+    args = [C.c_uint64(seed), _i64(count), _i64(lo), _i64(hi), _ptr(codes), C.c_int(codes.size),
+            _i64(p), _i64(split), _i64(blk[0]), _i64(blk[1]), _i64(blk[2])]
+    st = lib.ref_run_sweep(*args, C.c_void_p(), _i64(0), C.byref(n))
+    buf = C.create_string_buffer(n.value + 1)
+    st = st or lib.ref_run_sweep(*args, buf, _i64(n.value + 1), C.byref(n))
+    if st:
+        raise OracleError(st, "ref_run_sweep")
+    return buf.value.decode()
+
+
+def ref_simulate(strategy, param, m, n, k, bm, bn, bk, p, params=None):
+    """(makespan, utilization) of the reference's simulate (simulate.cpp:23-80)."""
+    lib = C.CDLL(REF_SO)
+    s = STRATEGIES[strategy] if isinstance(strategy, str) else int(strategy)
+    a, b, c, d = (params if params is not None else (0.0, 0.0, 1.0, 0.0))
+    ms, ut = C.c_double(), C.c_double()
+    st = lib.ref_simulate(C.c_int(s), _i64(param), _i64(m), _i64(n), _i64(k), _i64(bm), _i64(bn),
+                          _i64(bk), _i64(p), C.c_int(params is not None), C.c_double(a),
+                          C.c_double(b), C.c_double(c), C.c_double(d), C.byref(ms), C.byref(ut))
+    if st:
+        raise OracleError(st, "ref_simulate")
+    return ms.value, ut.value
+
+
 def ref_corpus_dims(seed: int, count: int, lo: int = 128, hi: int = 8192) -> np.ndarray:
     lib = C.CDLL(REF_SO)
     out = np.zeros((count, 3), np.int64)

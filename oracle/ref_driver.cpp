@@ -9,7 +9,8 @@
 //   streamk::to_text / from_text                              types.hpp:86-90
 //   streamk::random_matrix<T>                                 matrix.hpp:56-68
 //   streamk::gemm_reference<T> / execute<T>                   executor.hpp:22-207
-//   streamk::run_sweep (corpus order)                         sweep.hpp:29-33
+//   streamk::run_sweep (corpus order, full CSV)                sweep.hpp:29-33
+//   streamk::simulate / utilization                           simulate.hpp:34-40
 // Exceptions are mapped to status codes (invalid_argument=1, logic_error=4,
 // out_of_range=5, other=7).
 #include <cstdint>
@@ -22,6 +23,7 @@
 #include "streamk/decompose.hpp"
 #include "streamk/executor.hpp"
 #include "streamk/matrix.hpp"
+#include "streamk/simulate.hpp"
 #include "streamk/sweep.hpp"
 #include "streamk/types.hpp"
 
@@ -311,6 +313,52 @@ int ref_corpus_dims(uint64_t seed, int64_t count, int64_t lo, int64_t hi, int64_
       }
       ++i;
     }
+  });
+}
+
+// run_sweep's whole CSV text (sweep.cpp:75-112) for a corpus with one [lo, hi]
+// range on every axis; strategies as codes 0..4 (types.hpp:70 order).
+// *len = bytes needed (without the NUL); buf gets them when cap > *len.
+int ref_run_sweep(uint64_t seed, int64_t count, int64_t lo, int64_t hi, const int* strategies,
+                  int nstrat, int64_t p, int64_t split, int64_t bm, int64_t bn, int64_t bk,
+                  char* buf, int64_t cap, int64_t* len) {
+  return guarded([&] {
+    SweepSpec spec;
+    spec.m_lo = spec.n_lo = spec.k_lo = lo;
+    spec.m_hi = spec.n_hi = spec.k_hi = hi;
+    spec.sample_count = count;
+    spec.seed = seed;
+    spec.strategies.clear();
+    for (int i = 0; i < nstrat; ++i) spec.strategies.push_back(static_cast<Strategy>(strategies[i]));
+    spec.p = p;
+    spec.split = split;
+    std::ostringstream csv;
+    run_sweep(spec, {bm, bn, bk}, csv);
+    const std::string out = csv.str();
+    *len = static_cast<int64_t>(out.size());
+    if (buf && cap > *len) std::memcpy(buf, out.c_str(), out.size() + 1);
+  });
+}
+
+// simulate (simulate.cpp:23-69) of a closed-form schedule; with_params selects
+// CostParams{a, b, c, d}.  Writes makespan and utilization.
+int ref_simulate(int strategy, int64_t param, int64_t m, int64_t n, int64_t k, int64_t bm, int64_t bn,
+                 int64_t bk, int64_t p, int with_params, double a, double b, double c, double d,
+                 double* makespan, double* util) {
+  return guarded([&] {
+    const WorkAssignment wa = build(strategy, m, n, k, bm, bn, bk, param);
+    std::optional<CostParams> prm;
+    if (with_params) {
+      CostParams cp;
+      cp.a = a;
+      cp.b = b;
+      cp.c = c;
+      cp.d = d;
+      prm = cp;
+    }
+    const Timeline tl = simulate(wa, p, prm);
+    *makespan = tl.makespan;
+    *util = utilization(tl);
   });
 }
 

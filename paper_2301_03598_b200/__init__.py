@@ -40,7 +40,7 @@ __all__ = [
     "TileCoords", "CtaRange", "WorkAssignment", "tile_grid", "iter_to_coords", "data_parallel",
     "fixed_split", "stream_k", "hybrid", "fixup_peers_of", "quantization_efficiency", "to_text",
     "from_text", "kernel_blocking", "execute", "Gemm", "ProtocolError", "UnsupportedError",
-    "CudaError", "lib", "corpus",
+    "CudaError", "lib", "corpus", "simulate", "random_matrix_device", "reload_env",
 ]
 
 
@@ -84,7 +84,12 @@ class sk_gemm_desc(C.Structure):
         ("ldb", C.c_int64), ("C", C.c_void_p), ("ldc", C.c_int64),
         ("trace", C.c_void_p), ("cta_clocks", C.c_void_p), ("events", C.c_void_p),
         ("ranges", C.c_void_p), ("num_ranges", C.c_int64),
+        ("tile_group", C.c_int32), ("reserved0", C.c_int32),
     ]
+
+
+class sk_sim_params(C.Structure):
+    _fields_ = [("a", C.c_double), ("b", C.c_double), ("c", C.c_double), ("d", C.c_double)]
 
 
 SK_EXPLICIT = 5  # sk_strategy for an arbitrary range table (skb200.h)
@@ -136,6 +141,12 @@ _SIGS = {
     "sk_load_matrix_header": (C.c_int, [C.c_char_p, _P(C.c_int), _P(C.c_int64), _P(C.c_int64)]),
     "sk_load_matrix": (C.c_int, [C.c_char_p, C.c_int, C.c_int64, C.c_int64, C.c_void_p]),
     "sk_io_error": (C.c_char_p, []),
+    "sk_random_matrix": (C.c_int, [C.c_int, C.c_int32, C.c_uint64, C.c_int64, C.c_int64, C.c_int,
+                                   C.c_void_p, C.c_int64, C.c_void_p]),
+    "sk_simulate": (C.c_int, [_P(sk_problem), _P(sk_blocking), C.c_int, C.c_int64, C.c_void_p,
+                              C.c_int64, C.c_int64, C.c_void_p, _P(C.c_double), _P(C.c_double),
+                              C.c_void_p, C.c_int64, _P(C.c_int64)]),
+    "sk_reload_env": (None, []),
 }
 
 
@@ -554,6 +565,68 @@ def load_matrix(path: str, dtype: DType) -> np.ndarray:
     return out
 
 
+def reload_env() -> None:
+    """Re-read the SKB200_* tuning overrides (the library reads them once)."""
+    lib().sk_reload_env()
+
+
+def simulate(a: WorkAssignment, p: int, params=None, events: bool = False):
+    """The reference simulator (simulate.cpp:23-80) on this library's schedules:
+    returns (makespan, utilization) or, with events=True, a timeline.Timeline.
+    params: None (unit cost) or an object/dict with a, b, c, d (reference
+    CostParams semantics; e.g. fitted from device timelines)."""
+    from . import timeline as tlm
+
+    prm = None
+    if params is not None:
+        get = (lambda k: params[k]) if isinstance(params, dict) else (lambda k: getattr(params, k))
+        prm = sk_sim_params(get("a"), get("b"), get("c"), get("d"))
+    strategy, table = int(a.strategy), None
+    if a.param == 0:
+        table = _explicit_table(a)
+        strategy = SK_EXPLICIT
+    args = [C.byref(a.problem._c()), C.byref(a.blocking._c()), strategy, a.param,
+            table.ctypes.data_as(C.c_void_p) if table is not None else None,
+            0 if table is None else table.shape[0], p, C.byref(prm) if prm is not None else None]
+    ms, ut, n = C.c_double(), C.c_double(), C.c_int64()
+    st = lib().sk_simulate(*args, C.byref(ms), C.byref(ut), None, 0, C.byref(n))
+    if st not in (SK_OK,):
+        _check(st, "simulate")
+    if not events:
+        return ms.value, ut.value
+    ev = np.zeros((max(n.value, 1), 6), np.float64)
+    _check(lib().sk_simulate(*args, C.byref(ms), C.byref(ut), ev.ctypes.data_as(C.c_void_p), n.value,
+                             C.byref(n)), "simulate")
+    kinds = {0: "mac", 1: "fixup_wait", 2: "fixup_reduce"}
+    evs = [tlm.Event(int(r[0]), int(r[1]), kinds[int(r[2])], float(r[3]), float(r[4]), int(r[5]))
+           for r in ev[:n.value]]
+    return tlm.Timeline(p, evs, ms.value)
+
+
+_GEN = {DType.Int64: 0, DType.Float32: 1, DType.Float64: 2}
+
+
+def random_matrix_device(rows: int, cols: int, seed: int, gen: DType = DType.Float32,
+                         out: DType = DType.BFloat16, shift: int = 0, ld: Optional[int] = None,
+                         stream=None):
+    """random_matrix<gen>(rows, cols, seed) of the reference (matrix.hpp:39-68),
+    generated on the current CUDA device and rounded into `out` (a torch
+    tensor, rows x ld, viewed as rows x cols).  Int64 values may be shifted
+    right (arithmetic) by `shift`."""
+    import torch
+
+    tdt = {DType.BFloat16: torch.bfloat16, DType.Float16: torch.float16, DType.Float32: torch.float32,
+           DType.Float64: torch.float64}[DType(out)]
+    es = torch.tensor([], dtype=tdt).element_size()
+    al = 16 // es
+    ld = ld or -(-cols // al) * al
+    buf = torch.empty(rows, ld, dtype=tdt, device="cuda")
+    s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+    _check(lib().sk_random_matrix(_GEN[DType(gen)], shift, seed & (2**64 - 1), rows, cols, int(out),
+                                  C.c_void_p(buf.data_ptr()), ld, C.c_void_p(s)), "random_matrix")
+    return buf[:, :cols]
+
+
 def corpus(seed: int = 0, count: int = 32824, lo: int = 128, hi: int = 8192) -> np.ndarray:
     """The paper's log-sampled geometry corpus in run_sweep order
     (sweep.cpp:79-86): [count][4] uint64 rows of (m, n, k, matrix_seed)."""
@@ -580,8 +653,9 @@ def device_topology(device: int = 0) -> Optional[np.ndarray]:
     return die[:sms.value].copy() if ok.value else None
 
 
-def _launch_desc(a: WorkAssignment, ab_type: DType, variant: Variant):
+def _launch_desc(a: WorkAssignment, ab_type: DType, variant: Variant, tile_group: int = 0):
     d = sk_gemm_desc()
+    d.tile_group = tile_group
     d.problem, d.blocking = a.problem._c(), a.blocking._c()
     d.strategy, d.param = int(a.strategy), a.param
     table = _explicit_table(a) if a.param == 0 else None
@@ -611,10 +685,11 @@ def persistent_order(a: WorkAssignment, num_ctas: int, ab_type: DType = DType.BF
 
 
 def tile_blocks(a: WorkAssignment, ab_type: DType = DType.BFloat16,
-                variant: Variant = Variant.TwoSM) -> np.ndarray:
+                variant: Variant = Variant.TwoSM, tile_group: int = 0) -> np.ndarray:
     """[t][2] (tile row, tile column) of C each tile id denotes on the device
-    (sk_tile_block)."""
-    d, _table = _launch_desc(a, ab_type, variant)
+    (sk_tile_block): the reference's row-major map unless tile_group asks for
+    the grouped layout (sk_gemm_desc.tile_group)."""
+    d, _table = _launch_desc(a, ab_type, variant, tile_group)
     out = np.zeros((a.grid.total_tiles, 2), np.int64)
     r, c = C.c_int64(), C.c_int64()
     for t in range(a.grid.total_tiles):
@@ -695,7 +770,7 @@ class Gemm:
 
     def __init__(self, a: WorkAssignment, ab_type: DType = DType.BFloat16,
                  variant: Variant = Variant.Auto, num_ctas: int = 0, trace: bool = False,
-                 timeline: bool = False):
+                 timeline: bool = False, tile_group: int = 0):
         import torch  # device memory only
 
         self.a = a
@@ -714,6 +789,7 @@ class Gemm:
         d.param = a.param
         d.variant = int(variant)
         d.num_ctas = num_ctas
+        d.tile_group = tile_group  # 0: the reference's row-major tile -> C map
         d.lda, d.ldb, d.ldc = a.problem.k, a.problem.n, a.problem.n
         self.desc = d
         ws = C.c_size_t()
@@ -727,8 +803,10 @@ class Gemm:
         if trace:
             n = C.c_int64()
             _check(lib().sk_trace_size(C.byref(d), C.byref(n)), "trace_size")
+            # [4t tile records | g partial counts | t C-block storers]; -1 = unwritten
+            T = a.grid.total_tiles
             self.trace = torch.full((n.value,), -1, dtype=torch.int32, device="cuda")
-            self.trace[4 * a.grid.total_tiles:] = 0
+            self.trace[4 * T:n.value - T] = 0
         # per-CTA {clock64, globaltimer} stamps at start/end (clock_mhz())
         self.cta_clocks = torch.zeros(4 * 2 * 512, dtype=torch.int64, device="cuda") if trace else None
         self.events = None
@@ -736,6 +814,13 @@ class Gemm:
             n, stride = C.c_int64(), C.c_int64()
             _check(lib().sk_timeline_size(C.byref(d), C.byref(n), C.byref(stride)), "timeline_size")
             self.events = torch.zeros(8 * max(n.value, 1), dtype=torch.int64, device="cuda")
+
+    def block_storers(self) -> np.ndarray:
+        """[tiles_m][tiles_n] unit that stored each block of C in the last traced
+        launch (trace section 3; -1 = never stored)."""
+        T = self.a.grid.total_tiles
+        t = self.trace.cpu().numpy()
+        return t[t.size - T:].reshape(self.a.grid.tiles_m, self.a.grid.tiles_n)
 
     def timeline(self) -> np.ndarray:
         """Device-measured events of the last launch (timeline=True), one row per

@@ -20,8 +20,8 @@ CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(LIBDIR, "libskb200.so")
 
-SOURCES = ["skb200_api.cu", "sk_gemm_f16.cu", "sk_gemm_f64.cu", "sk_convert.cu", "sk_probe.cu",
-           "costmodel.cpp", "skmx.cpp"]
+SOURCES = ["skb200_api.cu", "sk_gemm_f16.cu", "sk_gemm_f64.cu", "sk_convert.cu", "sk_random.cu",
+           "sk_probe.cu", "costmodel.cpp", "skmx.cpp", "simulate.cpp"]
 HEADERS = ["ptx.cuh", "schedule.hpp", "sk_kernel_common.cuh", "exports.map"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

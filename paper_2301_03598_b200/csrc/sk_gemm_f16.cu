@@ -535,6 +535,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           t[1] = static_cast<int>(s.peer(tile, u, npeer));
           t[2] = static_cast<int>(u);
           t[3] = npeer;
+          // the block of C this unit stored (trace section 3, row-major blocks)
+          P.trace[4 * s.total_tiles + s.grid_size + tr * s.tiles_n + tc] = static_cast<int>(u);
         }
       }
       if (ev) {
@@ -590,21 +592,46 @@ size_t f16_slab_bytes() { return sizeof(float) * f16::SLAB_ELEMS; }
 int f16_stage_k() { return f16::BKS; }
 int f16_epilogue_warps() { return f16::EPI_WARPS; }
 
+// Per-device setup of variant CG on the CURRENT device (the caller holds the
+// device-state mutex and records that it ran): the dynamic-smem / cluster-size
+// opt-ins, then how many CTAs (1-SM) or CTA pairs (2-SM) can be co-resident --
+// the persistent grid is capped by it (a non-resident unit could be waited on).
+template <int CG>
+static cudaError_t prepare_cg(int sms, int* units) {
+  auto kern = f16::sk_gemm_f16<CG>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       f16::Cfg<CG>::alloc);
+  if (e != cudaSuccess) return e;
+  if (CG == 2) {
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(sms - sms % 2));
+    cfg.blockDim = dim3(f16::NUM_THREADS);
+    cfg.dynamicSmemBytes = f16::Cfg<CG>::alloc;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaOccupancyMaxActiveClusters(units, kern, &cfg);
+  }
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, f16::NUM_THREADS, f16::Cfg<CG>::alloc);
+  *units = per_sm * sms;
+  return e;
+}
+
+cudaError_t f16_prepare(int cg, int sms, int* units) {
+  return cg == 2 ? prepare_cg<2>(sms, units) : prepare_cg<1>(sms, units);
+}
+
 template <int CG>
 static cudaError_t launch_cg(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
                              const KernelParams& p, int pairs_or_ctas, cudaStream_t stream) {
-  static bool attr_set = false;  // guarded by the caller's device-init mutex
   auto kern = f16::sk_gemm_f16<CG>;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         f16::Cfg<CG>::alloc);
-    if (e != cudaSuccess) return e;
-    if (CG == 2) {
-      e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
-      if (e != cudaSuccess) return e;
-    }
-    attr_set = true;
-  }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(pairs_or_ctas * CG));
   cfg.blockDim = dim3(f16::NUM_THREADS);

@@ -221,16 +221,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
       if (tid == 0)
         for (int p = 1; p <= npeer; ++p) ptx::st_relaxed(P.flags + s.slab_of(s.peer(tile, u, p)), 0);
     }
+    // Clamped store of the owner's tile (executor.hpp:175-181).
+    int64_t tr, tc;
+    s.tile_rc(tile, &tr, &tc);
     if (tid == 0 && P.trace) {
       int* t = P.trace + 4 * tile;
       t[0] = static_cast<int>(u);
       t[1] = static_cast<int>(s.peer(tile, u, npeer));
       t[2] = static_cast<int>(u);
       t[3] = npeer;
+      P.trace[4 * s.total_tiles + s.grid_size + tr * s.tiles_n + tc] = static_cast<int>(u);
     }
-    // Clamped store of the owner's tile (executor.hpp:175-181).
-    int64_t tr, tc;
-    s.tile_rc(tile, &tr, &tc);
     const int64_t m0 = tr * BM, n0 = tc * BN;
 #pragma unroll
     for (int i = 0; i < 2; ++i)
@@ -266,6 +267,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
 
 size_t f64_slab_bytes() { return sizeof(double) * f64::SLAB_ELEMS; }
 
+// Per-device setup on the CURRENT device (the caller records that it ran).
 cudaError_t f64_max_ctas_per_sm(int* out) {
   cudaError_t e = cudaFuncSetAttribute(f64::sk_gemm_f64, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        f64::SMEM);

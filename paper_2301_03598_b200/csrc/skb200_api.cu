@@ -32,6 +32,7 @@ uint32_t make_idesc_f16(bool bf16, int M, int N);
 size_t f16_slab_bytes();
 int f16_stage_k();
 int f16_epilogue_warps();
+cudaError_t f16_prepare(int cg, int sms, int* units);
 cudaError_t launch_f16(int cg, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
                        const KernelParams& p, int grid, cudaStream_t stream);
 // sk_gemm_f64.cu
@@ -44,6 +45,9 @@ cudaError_t launch_convert(int kind, const void* src, int64_t ld_src, void* dst,
                            int64_t rows, int64_t cols, cudaStream_t stream);
 cudaError_t launch_f32_to_16(const float* src, void* dst, int64_t rows, int64_t cols,
                              int64_t ld_dst, bool bf16, cudaStream_t stream);
+// sk_random.cu
+cudaError_t launch_random_matrix(int gen, int out, uint64_t seed, int shift, int64_t rows, int64_t cols,
+                                 void* dst, int64_t ld, cudaStream_t stream);
 // sk_probe.cu
 bool probe_dies(int sms, std::vector<int>* die_of_sm, cudaError_t* cuda_err);
 }  // namespace skb200
@@ -82,9 +86,62 @@ struct DeviceInfo {
   // two-die topology (sk_probe.cu); probed once, outside stream capture
   bool topo_probed = false, topo_ok = false;
   std::vector<int> die_of_sm;
+  // Kernel attributes are per-device state: set once per device, together
+  // with the co-resident capacity of each persistent kernel (CTAs for the
+  // 1-SM and FP64 kernels, CTA pairs for the 2-SM kernel).  A persistent grid
+  // larger than that could leave an owner waiting on a unit whose CTA never
+  // becomes resident, so every launch is capped by it.
+  bool f16_ready[3] = {false, false, false};
+  int f16_units[3] = {0, 0, 0};
+  bool f64_ready = false;
+  int f64_per_sm = 0;
 };
 std::mutex g_dev_mu;
 DeviceInfo g_dev[64];
+
+// ---- tuning knobs ----------------------------------------------------------
+// SKB200_* environment overrides, read once (sk_reload_env re-reads them) so
+// a launch does not scan the environment ten times.  -1 = unset.
+struct Knobs {
+  int die_aware = 0, l2_promo = -1, raster_rows = -1, sk_first = -1, k_align = -1, coop = -1;
+  int pipeline = 1, pipe_g = -1, pipe_w = -1, pipe_trace = 0;
+  bool l2_policy_set = false;
+  int l2_policy[4] = {0, 0, 0, 0};
+};
+std::mutex g_knob_mu;
+Knobs g_knobs;
+bool g_knobs_loaded = false;
+
+Knobs read_knobs() {
+  Knobs k;
+  auto num = [](const char* name, int def) {
+    const char* e = getenv(name);
+    return e ? atoi(e) : def;
+  };
+  k.die_aware = num("SKB200_DIE_AWARE", 0);
+  k.l2_promo = num("SKB200_L2_PROMO", -1);
+  k.raster_rows = num("SKB200_RASTER_ROWS", -1);
+  k.sk_first = num("SKB200_SK_FIRST", -1);
+  k.k_align = num("SKB200_K_ALIGN", -1);
+  k.coop = num("SKB200_COOP", -1);
+  k.pipeline = num("SKB200_PIPELINE", 1);
+  k.pipe_g = num("SKB200_PIPE_G", -1);
+  k.pipe_w = num("SKB200_PIPE_W", -1);
+  k.pipe_trace = num("SKB200_PIPE_TRACE", 0);
+  if (const char* e = getenv("SKB200_L2_POLICY"))
+    k.l2_policy_set = sscanf(e, "%d,%d,%d,%d", &k.l2_policy[0], &k.l2_policy[1], &k.l2_policy[2],
+                             &k.l2_policy[3]) == 4;
+  return k;
+}
+
+const Knobs& knobs() {
+  std::lock_guard<std::mutex> lk(g_knob_mu);
+  if (!g_knobs_loaded) {
+    g_knobs = read_knobs();
+    g_knobs_loaded = true;
+  }
+  return g_knobs;
+}
 
 sk_status device_info(int dev, DeviceInfo* out) {
   if (dev < 0 || dev >= 64) return fail(SK_EINVAL, "device ordinal %d", dev);
@@ -108,8 +165,7 @@ bool die_table(int dev, cudaStream_t strm, int ranks, KernelParams* P) {
   // Opt-in (SKB200_DIE_AWARE=1): halves DRAM reads of isolated 8192^3 launches
   // (1.63 -> 0.99 GB, +6 % under ncu) but measured 1-4 % slower in back-to-back
   // bursts (profiles/r01/die_aware.txt), so the default schedule ignores dies.
-  const char* opt = getenv("SKB200_DIE_AWARE");
-  if (!opt || atoi(opt) == 0) return false;
+  if (!knobs().die_aware) return false;
   std::lock_guard<std::mutex> lk(g_dev_mu);
   DeviceInfo& d = g_dev[dev];
   if (!d.ok) return false;
@@ -167,8 +223,8 @@ sk_status make_tmap(CUtensorMap* m, CUtensorMapDataType dt, size_t esize, const 
   // 128-B L2 promotion: 8192^3 DP 1468.8 vs 1461.7 (256 B), hybrid 1445.4 vs
   // 1438.7 TFLOP/s; config 3 and skinny shapes unchanged (profiles/r01/l2_policy.txt).
   CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
-  if (const char* e = getenv("SKB200_L2_PROMO"))  // 0 none, 1 64B, 2 128B, 3 256B
-    promo = static_cast<CUtensorMapL2promotion>(atoi(e));
+  if (knobs().l2_promo >= 0)  // 0 none, 1 64B, 2 128B, 3 256B
+    promo = static_cast<CUtensorMapL2promotion>(knobs().l2_promo);
   CUresult r = fn(m, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, swz, promo,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -457,16 +513,22 @@ int64_t raster_rows_for(const sk_gemm_desc* d) {
   const double panel = static_cast<double>(d->blocking.blk_m) * static_cast<double>(d->problem.k) *
                        static_cast<double>(dtype_size(d->ab_type));
   int64_t rows = std::max<int64_t>(1, static_cast<int64_t>((32.0 * 1024 * 1024) / panel));
-  if (const char* e = getenv("SKB200_RASTER_ROWS")) rows = std::max(1, atoi(e));
-  return rows;
+  if (knobs().raster_rows > 0) rows = knobs().raster_rows;
+  // beyond the tile rows a group changes nothing; keeps group * tiles_n < 2^31
+  const int64_t tiles_m = ceil_div(d->problem.m, std::max<int64_t>(1, d->blocking.blk_m));
+  return std::max<int64_t>(1, std::min(rows, tiles_m));
 }
 
-// Grouped tile ids (see gemm_impl): G = the raster height, after which the
-// data-parallel raster is the identity.
-void apply_tile_group(Kernel kern, bool explicit_table, bool pipelined, Schedule* s, int64_t* raster) {
+// Tile id -> block of C (sk_gemm_desc.tile_group): the reference's row-major
+// map by default; grouped ids only on request (G = -1: the raster height),
+// after which the data-parallel raster is the identity.  G is clamped to
+// tiles_m (beyond it nothing changes, and G * tiles_n stays < 2^31).
+void apply_tile_group(const sk_gemm_desc* d, Kernel kern, bool explicit_table, bool pipelined,
+                      Schedule* s, int64_t* raster) {
+  s->tile_group = 1;
   if (pipelined || explicit_table || kern == Kernel::F64) return;
-  int64_t group = *raster;
-  if (const char* e = getenv("SKB200_TILE_GROUP")) group = std::max(1, atoi(e));
+  int64_t group = d->tile_group == -1 ? *raster : d->tile_group;
+  group = std::min<int64_t>(group, s->tiles_m);
   if (group > 1) {
     s->tile_group = group;
     *raster = 1;  // the id order already is the raster
@@ -480,7 +542,7 @@ void apply_tile_group(Kernel kern, bool explicit_table, bool pipelined, Schedule
 // profiles/r01/phase_order.txt).
 int phase_order_for(Kernel k) {
   int order = k == Kernel::F64 ? kSkFirst : kDpFirst;
-  if (const char* e = getenv("SKB200_SK_FIRST")) order = atoi(e);
+  if (knobs().sk_first >= 0) order = knobs().sk_first;
   return order;
 }
 }  // namespace
@@ -660,7 +722,7 @@ sk_status sk_trace_size(const sk_gemm_desc* d, int64_t* ints) {
   Schedule s;
   sk_status st = check_desc(d, &k, &s);
   if (st) return st;
-  if (ints) *ints = 4 * s.total_tiles + s.grid_size;
+  if (ints) *ints = 5 * s.total_tiles + s.grid_size;
   return SK_OK;
 }
 
@@ -721,7 +783,7 @@ sk_status sk_persistent_order(const sk_gemm_desc* d, int64_t num_ctas, int64_t c
   if (num_ctas < 1 || cta < 0 || cta >= num_ctas || !count || (max_records > 0 && !out))
     return fail(SK_EINVAL, "persistent_order: bad grid / cta / output");
   int64_t raster = raster_rows_for(d);
-  apply_tile_group(kern, s.strategy == kExplicit, false, &s, &raster);
+  apply_tile_group(d, kern, s.strategy == kExplicit, false, &s, &raster);
   SegmentIter it(s, cta, num_ctas, default_lane(s, cta, num_ctas), raster, phase_order_for(kern));
   int64_t n = 0, u, tile, lb, le;
   while (it.next(s, &u, &tile, &lb, &le)) {
@@ -743,13 +805,27 @@ sk_status sk_tile_block(const sk_gemm_desc* d, int64_t tile, int64_t* tile_row, 
   if (!tile_row || !tile_col) return fail(SK_EINVAL, "null output");
   if (tile < 0 || tile >= s.total_tiles) return fail(SK_ERANGE, "tile %lld out of range", (long long)tile);
   int64_t raster = raster_rows_for(d);
-  apply_tile_group(kern, s.strategy == kExplicit, false, &s, &raster);
+  apply_tile_group(d, kern, s.strategy == kExplicit, false, &s, &raster);
   s.tile_rc(tile, tile_row, tile_col);
   return SK_OK;
 }
 
 sk_status sk_gemm(const sk_gemm_desc* d, void* ws, size_t ws_bytes, void* stream) {
   return gemm_impl(d, ws, ws_bytes, static_cast<cudaStream_t>(stream));
+}
+
+sk_status sk_random_matrix(sk_dtype gen_type, int32_t shift, uint64_t seed, int64_t rows, int64_t cols,
+                           sk_dtype out_type, void* dst, int64_t ld, void* stream) {
+  if (rows < 0 || cols < 0 || ld < cols || shift < 0 || shift > 7 || (rows * cols > 0 && !dst))
+    return fail(SK_EINVAL, "random_matrix: bad extents / buffer");
+  const int gen = gen_type == SK_INT64 ? 0 : gen_type == SK_FLOAT32 ? 1 : gen_type == SK_FLOAT64 ? 2 : -1;
+  const int out = out_type == SK_BFLOAT16 ? 0 : out_type == SK_FLOAT16 ? 1 : out_type == SK_FLOAT32 ? 2
+                  : out_type == SK_FLOAT64 ? 3 : -1;
+  if (gen < 0 || out < 0 || (gen == 2 && out < 2))
+    return fail(SK_EINVAL, "random_matrix: unsupported generator / output type pair");
+  if (rows * cols == 0) return SK_OK;
+  SK_CUDA(launch_random_matrix(gen, out, seed, shift, rows, cols, dst, ld, static_cast<cudaStream_t>(stream)));
+  return SK_OK;
 }
 
 }  // extern "C"
@@ -823,7 +899,7 @@ sk_status gemm_impl(const sk_gemm_desc* d, void* ws, size_t ws_bytes, cudaStream
   // kept near 32 MB so they stay L2-resident while B streams through; measured
   // best at 8192^3: 16 rows (1-SM), 8 rows (2-SM) (profiles/r01/raster_rows.txt).
   P.raster_rows = raster > 0 ? raster : raster_rows_for(d);
-  apply_tile_group(kern, xp, a_ready != nullptr, &P.s, &P.raster_rows);
+  apply_tile_group(d, kern, xp, a_ready != nullptr, &P.s, &P.raster_rows);
   // Grouped tile ids (Schedule::tile_rc): the same G-row groups now also
   // decide which block of C each tile id denotes, so a hybrid's trailing
   // Stream-K region is a compact 8 x 17 block at 8192^3 instead of a
@@ -851,12 +927,38 @@ sk_status gemm_impl(const sk_gemm_desc* d, void* ws, size_t ws_bytes, cudaStream
   // panels are shared in time across the SK region; 8192^3 hybrid 1458 -> 1482
   // TFLOP/s, config-3 geomean 1.287 -> 1.325 (profiles/r01/k_align.txt).
   P.k_align = kern == Kernel::F64 ? 0 : 1;
-  if (const char* e = getenv("SKB200_K_ALIGN")) P.k_align = atoi(e);
-  if (const char* e = getenv("SKB200_L2_POLICY"))
-    sscanf(e, "%d,%d,%d,%d", &P.l2_policy[0], &P.l2_policy[1], &P.l2_policy[2], &P.l2_policy[3]);
+  if (knobs().k_align >= 0) P.k_align = knobs().k_align;
+  if (knobs().l2_policy_set)
+    for (int i = 0; i < 4; ++i) P.l2_policy[i] = knobs().l2_policy[i];
+  // Persistent grid: at most the co-resident capacity of the kernel on this
+  // device (queried once per device with the kernel attributes, which are
+  // per-device state), so every unit a fixup wait points to is running.
+  int resident = 0;
+  {
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    DeviceInfo& di = g_dev[dev];
+    if (kern == Kernel::F64) {
+      if (!di.f64_ready) {
+        cudaError_t e = f64_max_ctas_per_sm(&di.f64_per_sm);
+        if (e != cudaSuccess) return cuda_fail(e, "sk_gemm_f64 occupancy");
+        if (di.f64_per_sm < 1) return fail(SK_ECUDA, "sk_gemm_f64 does not fit on an SM");
+        di.f64_ready = true;
+      }
+      resident = di.f64_per_sm * info.sms;
+    } else {
+      const int cg = kern == Kernel::F16_2SM ? 2 : 1;
+      if (!di.f16_ready[cg]) {
+        cudaError_t e = f16_prepare(cg, info.sms, &di.f16_units[cg]);
+        if (e != cudaSuccess) return cuda_fail(e, "sk_gemm_f16 attributes / occupancy");
+        if (di.f16_units[cg] < 1) return fail(SK_ECUDA, "sk_gemm_f16 does not fit on the device");
+        di.f16_ready[cg] = true;
+      }
+      resident = std::min(di.f16_units[cg], info.sms / P.ranks);
+    }
+  }
   const int64_t units = std::max<int64_t>(s.grid_size, 1);
-  const int64_t cap = d->num_ctas > 0 ? d->num_ctas : info.sms / P.ranks;
-  P.num_ctas = std::min<int64_t>(units, std::min<int64_t>(cap, info.sms / P.ranks));
+  const int64_t cap = d->num_ctas > 0 ? d->num_ctas : resident;
+  P.num_ctas = std::min<int64_t>(units, std::min<int64_t>(cap, resident));
   // Die-aware data-parallel phase: needs every SM (pair) in the persistent grid,
   // so each die's lane ranks are dense (dp_lane); the rasterised DP order is
   // otherwise unchanged.
@@ -872,7 +974,7 @@ sk_status gemm_impl(const sk_gemm_desc* d, void* ws, size_t ws_bytes, cudaStream
   P.coop = 0;
   if (coop_tiles(kern, s) >= 0 && s.bal.count <= P.num_ctas && !a_ready && !c_done) {
     P.coop = mean_contributors(s) >= 8.0 ? 1 : 0;
-    if (const char* e = getenv("SKB200_COOP")) P.coop = atoi(e) != 0;
+    if (knobs().coop >= 0) P.coop = knobs().coop != 0;
   }
   P.die_aware = 0;
   if ((kern == Kernel::F16_1SM || kern == Kernel::F16_2SM) && s.dp_tiles > 0 &&
@@ -895,11 +997,7 @@ sk_status gemm_impl(const sk_gemm_desc* d, void* ws, size_t ws_bytes, cudaStream
                    d->ldc, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B);
     if (st) return st;
     P.idesc = make_idesc_f16(d->ab_type == SK_BFLOAT16, 128 * cg, 256);
-    cudaError_t e;
-    {
-      std::lock_guard<std::mutex> lk(g_dev_mu);
-      e = launch_f16(cg, ta, tb, tc, P, static_cast<int>(P.num_ctas), strm);
-    }
+    const cudaError_t e = launch_f16(cg, ta, tb, tc, P, static_cast<int>(P.num_ctas), strm);
     if (e != cudaSuccess) return cuda_fail(e, cg == 2 ? "sk_gemm_f16<2> launch" : "sk_gemm_f16<1> launch");
     return SK_OK;
   }
@@ -911,19 +1009,8 @@ sk_status gemm_impl(const sk_gemm_desc* d, void* ws, size_t ws_bytes, cudaStream
     st = make_tmap(&tb, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, d->B, d->problem.k, d->problem.n,
                    d->ldb, 16, 16, CU_TENSOR_MAP_SWIZZLE_128B);
     if (st) return st;
-    cudaError_t e;
-    {
-      std::lock_guard<std::mutex> lk(g_dev_mu);
-      static int occ = 0;  // co-resident CTAs per SM (persistent grid must fit in one wave)
-      if (occ == 0) {
-        e = f64_max_ctas_per_sm(&occ);
-        if (e != cudaSuccess) return cuda_fail(e, "sk_gemm_f64 occupancy");
-        if (occ < 1) return fail(SK_ECUDA, "sk_gemm_f64 does not fit on an SM");
-      }
-      const int64_t cap64 = d->num_ctas > 0 ? d->num_ctas : static_cast<int64_t>(info.sms) * occ;
-      P.num_ctas = std::min<int64_t>(units, std::min<int64_t>(cap64, static_cast<int64_t>(info.sms) * occ));
-      e = launch_f64(ta, tb, static_cast<double*>(d->C), d->ldc, P, static_cast<int>(P.num_ctas), strm);
-    }
+    const cudaError_t e =
+        launch_f64(ta, tb, static_cast<double*>(d->C), d->ldc, P, static_cast<int>(P.num_ctas), strm);
     if (e != cudaSuccess) return cuda_fail(e, "sk_gemm_f64 launch");
     return SK_OK;
   }
@@ -1049,8 +1136,8 @@ sk_status execute_pipelined(ExecCache& X, sk_gemm_desc& d, size_t ws_bytes, cons
   // the call is bound by bidirectional PCIe, not by when C starts to leave.
   int64_t G = f64 ? 1 : 8, W = f64 ? cols : 8;
   if (!f64) {
-    if (const char* e = getenv("SKB200_PIPE_G")) G = std::max(1, atoi(e));
-    if (const char* e = getenv("SKB200_PIPE_W")) W = std::max(1, atoi(e));
+    if (knobs().pipe_g > 0) G = knobs().pipe_g;
+    if (knobs().pipe_w > 0) W = knobs().pipe_w;
   }
   pf.raster = std::min<int64_t>(rows, G);
   pf.g = static_cast<int>(pf.raster);
@@ -1160,8 +1247,7 @@ sk_status execute_pipelined(ExecCache& X, sk_gemm_desc& d, size_t ws_bytes, cons
   if (zero_c) SK_CUDA(cudaMemsetAsync(X.buf[2], 0, static_cast<size_t>(m * d.ldc) * csz, sm));
   // SKB200_PIPE_TRACE=1: event after every copy and the kernel, printed to
   // stderr in ms from the call's start (profiles/r01d/pipeline_blocks.txt)
-  const char* tr_env = getenv("SKB200_PIPE_TRACE");
-  const bool trace = tr_env && atoi(tr_env) != 0;
+  const bool trace = knobs().pipe_trace != 0;
   std::vector<std::pair<std::string, cudaEvent_t>> tev;
   auto mark = [&](const std::string& what, cudaStream_t q) {
     if (!trace) return;
@@ -1219,7 +1305,18 @@ sk_status execute_pipelined(ExecCache& X, sk_gemm_desc& d, size_t ws_bytes, cons
   const uint8_t* Cd = static_cast<const uint8_t*>(X.buf[2]);
   PFN_waitValue32 wv = wait_value32();
   for (int64_t b : out_order) {
-    if (!target[static_cast<size_t>(b)]) continue;  // nothing stores it (explicit tables)
+    if (!target[static_cast<size_t>(b)]) {
+      // nothing stores this block (explicit tables that leave tiles unstarted):
+      // the reference returns zeros there (its fresh C, matrix.hpp:22)
+      if (zero_c) {
+        const int64_t r0 = (b / pf.np) * pf.g * bm, nr = std::min(r0 + pf.g * bm, m) - r0;
+        const int64_t c0 = (b % pf.np) * pf.w * bn, nc = std::min(c0 + pf.w * bn, n) - c0;
+        uint8_t* Cz = static_cast<uint8_t*>(C);
+        for (int64_t r = r0; r < r0 + nr; ++r)
+          memset(Cz + static_cast<size_t>(r * n + c0) * csz, 0, static_cast<size_t>(nc) * csz);
+      }
+      continue;
+    }
     const CUresult cr = wv(reinterpret_cast<CUstream>(so), reinterpret_cast<CUdeviceptr>(c_done + b),
                            target[static_cast<size_t>(b)], CU_STREAM_WAIT_VALUE_GEQ);
     if (cr != CUDA_SUCCESS) return fail(SK_ECUDA, "cuStreamWaitValue32 failed (%d)", int(cr));
@@ -1328,8 +1425,7 @@ sk_status execute_impl(const sk_problem* p, const sk_blocking* b, sk_strategy st
   // Overlapped transfers: pinned host buffers, no element conversion, > 1 tile row.
   {
     const bool same = is16 ? host_type == compute_type : host_type == SK_FLOAT64;
-    const char* e = getenv("SKB200_PIPELINE");
-    if (same && !(e && atoi(e) == 0) && m > b->blk_m && wait_value32() && write_value32() && is_pinned(A) &&
+    if (same && knobs().pipeline != 0 && m > b->blk_m && wait_value32() && write_value32() && is_pinned(A) &&
         is_pinned(B) && is_pinned(C))
       return execute_pipelined(X, d, ws_bytes, A, B, C, esz, csz, zero_c);
   }
@@ -1392,3 +1488,9 @@ extern "C" sk_status sk_execute_ranges(const sk_problem* p, const sk_blocking* b
 }
 
 extern "C" void sk_execute_release(void) { g_exec.release(); }
+
+extern "C" void sk_reload_env(void) {
+  std::lock_guard<std::mutex> lk(g_knob_mu);
+  g_knobs = read_knobs();
+  g_knobs_loaded = true;
+}

@@ -51,7 +51,7 @@ def test_sass_is_tcgen05_and_tma(sk):
 
 def test_status_strings_and_version(sk):
     lib = sk.lib()
-    assert lib.sk_abi_version() == 2  # v2: SK_EXPLICIT range tables
+    assert lib.sk_abi_version() == 3  # v2: SK_EXPLICIT range tables; v3: tile_group
     for code in range(7):
         assert lib.sk_status_string(code)
 

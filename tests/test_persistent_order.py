@@ -110,23 +110,22 @@ def _dp_unit(sk, a, u):
 
 @pytest.mark.parametrize("shape,blk", CASES + [((8192, 8192, 64), (256, 256, 64)),
                                                ((4000, 300, 777), (128, 256, 64))])
-def test_tile_blocks_bijection(sk, shape, blk, monkeypatch):
-    """Grouped tile ids (Schedule::tile_rc) denote every block of C exactly once;
-    SKB200_TILE_GROUP=1 and the FP64 kernel keep the reference's row-major map
-    (executor.hpp:69-70)."""
+def test_tile_blocks_bijection(sk, shape, blk):
+    """The default tile id -> block of C map is the reference's row-major one
+    (executor.hpp:69-70, 173-174) on every kernel; the opt-in grouped layout
+    (sk_gemm_desc.tile_group = G or -1) still denotes every block exactly once."""
     problem = sk.GemmProblem(*shape)
     b = sk.BlockingFactors(*blk)
     variant = sk.Variant.TwoSM if blk[0] == 256 else sk.Variant.OneSM
     a = sk.stream_k(problem, b, 74)
     tm, tn = a.grid.tiles_m, a.grid.tiles_n
     row_major = np.array([(t // tn, t % tn) for t in range(tm * tn)])
-    blocks = sk.tile_blocks(a, variant=variant)
-    assert sorted(map(tuple, blocks.tolist())) == sorted(map(tuple, row_major.tolist()))
-    monkeypatch.setenv("SKB200_TILE_GROUP", "1")
     assert np.array_equal(sk.tile_blocks(a, variant=variant), row_major)
-    monkeypatch.delenv("SKB200_TILE_GROUP")
+    for g in (-1, 3, 10 ** 6):  # raster height, explicit, clamped to tiles_m
+        blocks = sk.tile_blocks(a, variant=variant, tile_group=g)
+        assert sorted(map(tuple, blocks.tolist())) == sorted(map(tuple, row_major.tolist()))
     b64 = sk.kernel_blocking(sk.DType.Float64)
     a64 = sk.stream_k(problem, b64, 296)
     t64 = a64.grid.tiles_n
     want = np.array([(t // t64, t % t64) for t in range(a64.grid.total_tiles)])
-    assert np.array_equal(sk.tile_blocks(a64, sk.DType.Float64, sk.Variant.Auto), want)
+    assert np.array_equal(sk.tile_blocks(a64, sk.DType.Float64, sk.Variant.Auto, tile_group=-1), want)
