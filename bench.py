@@ -13,12 +13,13 @@ steps).  Rank 0 prints ONE JSON line.
 
 Multi-GPU (torchrun, one process per GPU): weak scaling with no data-path
 collective -- rank r computes its own N-column block C[:, r*n:(r+1)*n] of a
-GEMM with N*n columns; the only collectives are the timing barrier and the
-max-over-ranks reduction.
+GEMM with N*n columns.  No NCCL anywhere: the control plane (the timing
+barrier and the max-over-ranks reduction) runs over gloo on host tensors.
 
 --impl reference times the reference's own CPU executor (streamk::execute<float>,
 oracle/_ref, built from the reference sources) on rank 0 on a bounded row
-sample of the same workload, with all host threads.
+sample of the same workload, with all host threads; the product arm's
+cpu_baseline times the same sample.
 """
 from __future__ import annotations
 
@@ -42,7 +43,7 @@ METRIC = ("GEMM TFLOP/s and % of B200 tensor peak; geomean speedup of Stream-K v
           "data-parallel")
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
@@ -55,11 +56,53 @@ def parse():
     ap.add_argument("--k", type=int, default=8192)
     ap.add_argument("--dtype", default="bf16", choices=["bf16", "fp16", "fp64"])
     ap.add_argument("--variant", default="2sm", choices=["auto", "1sm", "2sm"])
+    ap.add_argument("--tile-group", type=int, default=0,
+                    help="sk_gemm_desc.tile_group: 0 = the reference's row-major tile map (default); "
+                         "G > 1 / -1 = opt-in grouped layout (experiments)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--cpu-rows", type=int, default=0, help="row sample for the CPU legs (0=auto)")
-    return ap.parse_args()
+    ap.add_argument("--sustained-s", type=float, default=2.0,
+                    help="seconds of back-to-back launches for the sustained figure (0 = skip)")
+    return ap.parse_args(argv)
+
+
+class ControlPlane:
+    """Barrier + max-over-ranks over gloo (host tensors): the only inter-rank
+    traffic of the bench.  The GEMM data path has no collective and no NCCL."""
+
+    def __init__(self, world: int):
+        self.world = world
+        self.dist = None
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.init_process_group("gloo")
+            self.dist = dist
+
+    def barrier(self):
+        if self.dist:
+            self.dist.barrier()
+
+    def max(self, x: float) -> float:
+        if not self.dist:
+            return x
+        import torch
+
+        t = torch.tensor([x], dtype=torch.float64)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def close(self):
+        if self.dist:
+            self.dist.barrier()
+            self.dist.destroy_process_group()
+
+
+# Row sample of the CPU legs: both the reference arm (per step) and the
+# product arm's cpu_baseline time streamk::execute on these many rows of A.
+CPU_ROWS = {"bf16": 1024, "fp16": 1024, "fp64": 512}
 
 
 def load_peaks():
@@ -69,6 +112,14 @@ def load_peaks():
         return float(p["bf16_tflops"]), float(p.get("hbm_gbs", 6552.3)), "measured"
     except Exception:
         return 1590.0, 6650.0, "fallback"
+
+
+def load_sustained_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["bf16_tflops_sustained"])
+    except Exception:
+        return None
 
 
 def load_traffic(workload: str):
@@ -163,7 +214,7 @@ def cpu_reference_leg(args, strategy, param, blk, rows=None):
     orc = oracle.Oracle(kind)
     threads = os.cpu_count() or 1
     fp64 = args.dtype == "fp64"
-    rows = rows or args.cpu_rows or (1536 if fp64 else 3072)
+    rows = rows or args.cpu_rows or CPU_ROWS[args.dtype]
     m, n, k = rows, args.n, args.k
     dt_name, tname = ("float64", "double") if fp64 else ("float32", "float")
     A = orc.random_matrix(m, k, 42, dt_name)
@@ -194,7 +245,7 @@ def run_reference_arm(args, rank, world):
     vals = []
     last = None
     for i in range(args.warmup + args.steps):
-        tf, dt, sample, cores, kind = cpu_reference_leg(args, strategy, param, blk, rows=args.cpu_rows or 128)
+        tf, dt, sample, cores, kind = cpu_reference_leg(args, strategy, param, blk)
         if i >= args.warmup:
             vals.append(tf)
         last = (sample, cores, kind)
@@ -228,23 +279,11 @@ def main():
     import paper_2301_03598_b200 as sk
 
     ndev = torch.cuda.device_count()
-    # One rank per GPU.  More ranks than GPUs only happens when the multi-rank
-    # path is exercised on a 1-GPU box: ranks then share devices and the two
-    # timing collectives (barrier, max-reduction) use gloo, since NCCL refuses
-    # two ranks on one GPU.  The GEMM data path has no collective either way.
+    # One rank per GPU (more ranks than GPUs only when the multi-rank path is
+    # exercised on a 1-GPU box: ranks then share the device).
     local = local % max(ndev, 1)
     torch.cuda.set_device(local)
-    dist = None
-    coll_dev = "cuda"
-    if world > 1:
-        import torch.distributed as dist_
-
-        if world <= ndev:
-            dist_.init_process_group("nccl", device_id=torch.device("cuda", local))
-        else:
-            dist_.init_process_group("gloo")
-            coll_dev = "cpu"
-        dist = dist_
+    cp = ControlPlane(world)
 
     ab = {"bf16": sk.DType.BFloat16, "fp16": sk.DType.Float16, "fp64": sk.DType.Float64}[args.dtype]
     tdt = {"bf16": torch.bfloat16, "fp16": torch.float16, "fp64": torch.float64}[args.dtype]
@@ -261,60 +300,110 @@ def main():
     a = sk._assignment(strategy, problem, blk, param)
     a_dp = sk.data_parallel(problem, blk)
 
-    g = torch.Generator(device="cuda").manual_seed(1234 + rank)
-    A = (torch.rand(m, k, device="cuda", generator=g) * 2 - 1).to(tdt)
-    B = (torch.rand(k, n, device="cuda", generator=g) * 2 - 1).to(tdt)
+    # The reference's inputs (random_matrix<float>, matrix.hpp:56-68), generated
+    # on the device and rounded to the kernel's input type.
+    gen = sk.DType.Float64 if args.dtype == "fp64" else sk.DType.Float32
+    A = sk.random_matrix_device(m, k, 42 + 2 * rank, gen, ab)
+    B = sk.random_matrix_device(k, n, 43 + 2 * rank, gen, ab)
     Cout = torch.empty(m, n, device="cuda", dtype=cdt)
-    gemm = sk.Gemm(a, ab, variant)
-    gemm_dp = sk.Gemm(a_dp, ab, variant)
+    gemm = sk.Gemm(a, ab, variant, tile_group=args.tile_group)
+    gemm_dp = sk.Gemm(a_dp, ab, variant, tile_group=args.tile_group)
     stream = torch.cuda.current_stream()
     flops = 2.0 * m * n * k
 
-    def timed(gm, steps, warmup):
+    def timed(run, steps, warmup):
         for _ in range(warmup):
-            gm.run(A, B, Cout)
+            run()
         torch.cuda.synchronize()
-        if dist:
-            dist.barrier()
+        cp.barrier()
         torch.cuda.synchronize()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(steps):
-            gm.run(A, B, Cout)
+            run()
         e1.record(stream)
         torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1) / steps
-        if dist:
-            t = torch.tensor([ms], device=coll_dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms = float(t.item())
-        return ms
+        return cp.max(e0.elapsed_time(e1) / steps)
 
+    run_sk = lambda: gemm.run(A, B, Cout)  # noqa: E731
     with ClockSampler(local) as clk:
-        ms = timed(gemm, args.steps, max(args.warmup, 3))
+        ms = timed(run_sk, args.steps, max(args.warmup, 3))
     gemm.check()
     clocks = clk.summary()
     # Cross-check with the clock the kernel itself sees: clock64 / globaltimer
     # stamped by every CTA of a traced launch run back-to-back after the timed
     # region (same power state).
-    traced = sk.Gemm(a, ab, variant, trace=True)
+    traced = sk.Gemm(a, ab, variant, trace=True, tile_group=args.tile_group)
     for _ in range(max(3, min(args.steps, 10))):
         traced.run(A, B, Cout)
     torch.cuda.synchronize()
     clocks["kernel_sm_mhz"] = traced.clock_mhz()
     del traced
-    ms_dp = timed(gemm_dp, max(args.steps // 2, 3), 3)
+    ms_dp = timed(lambda: gemm_dp.run(A, B, Cout), max(args.steps // 2, 3), 3)
     gemm_dp.check()
 
     value = flops * world / (ms * 1e-3) / 1e12  # whole-job TFLOP/s
     per_launch_tflops = flops / (ms * 1e-3) / 1e12
     peak_tf, _, peak_kind = load_peaks()
     peak_kind = f"{peak_kind} bf16_tflops (burst)"
-    if args.dtype == "fp64":  # no measured FP64 peak in MEASURED_PEAKS.json: datasheet
-        peak_tf, peak_kind = 40.0, "datasheet B200 FP64 tensor (40 TFLOP/s)"
+    sustained_peak = load_sustained_peak()
+    cublas = None
+    if args.dtype == "fp64":
+        # no FP64 figure in MEASURED_PEAKS.json: cuBLAS DGEMM of the same shape,
+        # measured here (best of 5), is the FP64 denominator
+        dg = lambda: torch.matmul(A, B)  # noqa: E731
+        ms_d = min(timed(dg, 3, 2) for _ in range(5))
+        peak_tf, peak_kind = flops / (ms_d * 1e-3) / 1e12, "measured cuBLAS DGEMM, same shape and harness"
+        sustained_peak = None
     esz = A.element_size()
     workload = f"{m}x{n}x{k}_{args.dtype}_{sk.strategy_name(strategy)}_{blk.blk_m}x{blk.blk_n}x{blk.blk_k}"
+
+    # ---- sustained: back-to-back launches for >= sustained_s seconds, own clocks
+    sustained = None
+    if args.sustained_s > 0:
+        reps = max(args.steps, int(math.ceil(args.sustained_s * 1e3 / ms)))
+        with ClockSampler(local) as clk2:
+            ms_s = timed(run_sk, reps, 3)
+        gemm.check()
+        tf_s = flops / (ms_s * 1e-3) / 1e12
+        sustained = {"tflops": tf_s, "launches": reps, "seconds": reps * ms_s * 1e-3,
+                     "clocks": clk2.summary()}
+        if sustained_peak:
+            sustained.update(peak=sustained_peak, frac=tf_s / sustained_peak,
+                             peak_kind="measured bf16_tflops_sustained")
+        if args.dtype != "fp64" and rank == 0:
+            # the library GEMM on the same operands in the same harness, for context
+            mm = lambda: torch.matmul(A, B)  # noqa: E731
+            cb = min(timed(mm, 10, 3) for _ in range(3))
+            cs = timed(mm, reps, 3)
+            cublas = {"burst_tflops": flops / (cb * 1e-3) / 1e12,
+                      "sustained_tflops": flops / (cs * 1e-3) / 1e12,
+                      "what": "torch.matmul (cuBLAS, bf16 C), same operands, for comparison only"}
+
+    # ---- host cost of one sk_gemm call (descriptor checks, cached tensor maps,
+    # launch), outside CUDA graphs, on a short shape
+    host = None
+    if rank == 0:
+        hp = sk.GemmProblem(512, 512, 512)
+        hg = sk.Gemm(sk.stream_k(hp, blk, p_dev), ab, variant)
+        hA = sk.random_matrix_device(512, 512, 1, gen, ab)
+        hB = sk.random_matrix_device(512, 512, 2, gen, ab)
+        hC = torch.empty(512, 512, device="cuda", dtype=cdt)
+        for _ in range(20):
+            hg.run(hA, hB, hC)
+        torch.cuda.synchronize()
+        calls = 500
+        t0 = time.perf_counter()
+        for _ in range(calls):
+            hg.run(hA, hB, hC)
+        host_us = (time.perf_counter() - t0) / calls * 1e6
+        torch.cuda.synchronize()
+        ms_small = timed(lambda: hg.run(hA, hB, hC), 200, 10)
+        hg.check()
+        host = {"shape": [512, 512, 512], "strategy": f"stream_k({p_dev})",
+                "host_us_per_call": host_us, "device_us_per_launch_back_to_back": ms_small * 1e3,
+                "path": "Gemm.run -> sk_gemm (ctypes), no CUDA graph"}
 
     # ---- end to end through the reference-facing C-ABI call (sk_execute): pinned
     # host A/B in, host C out, copies inside the timed region.
@@ -340,17 +429,12 @@ def main():
 
         for _ in range(2):
             e2e_step()
-        if dist:
-            dist.barrier()
+        cp.barrier()
         steps_e2e = max(3, min(args.steps, 5))
         t0 = time.perf_counter()
         for _ in range(steps_e2e):
             e2e_step()  # synchronous: H2D + kernel + D2H + status read
-        dt = (time.perf_counter() - t0) / steps_e2e
-        if dist:
-            t = torch.tensor([dt], device=coll_dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            dt = float(t.item())
+        dt = cp.max((time.perf_counter() - t0) / steps_e2e)
         e2e = {"value": flops * world / dt / 1e12, "unit": "TFLOP/s",
                "h2d_bytes_per_step": int(A.numel() * A.element_size() + B.numel() * B.element_size()),
                "d2h_bytes_per_step": int(Cout.numel() * Cout.element_size() + 4),
@@ -393,10 +477,14 @@ def main():
             "metric": METRIC, "value": value, "unit": "TFLOP/s",
             "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3),
             "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": args.dtype, "data": "synthetic uniform[-1,1) on device",
+            "vs_baseline": None, "dtype": args.dtype,
+            "data": "synthetic: the reference's random_matrix<float>(42 + 2r), (43 + 2r) rounded to "
+                    f"{args.dtype}, generated on the device",
             "config": {"workload": workload, "m": m, "n": n * world, "k": k,
                        "n_per_gpu": n, "strategy": sk.strategy_name(strategy), "param": param,
                        "grid_size": a.grid_size, "blocking": [blk.blk_m, blk.blk_n, blk.blk_k],
+                       "tile_map": "row-major (executor.hpp:69-70)" if args.tile_group in (0, 1)
+                       else f"grouped (tile_group={args.tile_group}, opt-in)",
                        "parallelism": f"column-blocks x{world}, no collective",
                        "l2": "inputs 256 MiB > 126 MB L2 (no flush needed)"},
             "pct_of_peak": {"measured_cublas_burst": per_launch_tflops / peak_tf,
@@ -410,16 +498,17 @@ def main():
                          "algorithmic": {"flops_per_launch": flops,
                                          "bytes_per_launch": esz * (m * k + k * n)
                                          + Cout.element_size() * m * n}},
+            "sustained": sustained,
+            "cublas_same_harness": cublas,
             "clocks": clocks,
             "gpu_launches": args.steps,
+            "host_overhead": host,
             "e2e": e2e,
             "cpu_baseline": cpu,
             "stream_k_vs_dp": sweep,
         }
         print(json.dumps(line), flush=True)
-    if dist:
-        dist.barrier()
-        dist.destroy_process_group()
+    cp.close()
 
 
 if __name__ == "__main__":

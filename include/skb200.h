@@ -250,6 +250,12 @@ sk_status sk_persistent_order(const sk_gemm_desc* desc, int64_t num_ctas, int64_
  * launch of `desc`: row-major like executor.hpp:69-70 unless desc->tile_group
  * selects the grouped layout (tcgen05 kernels, closed-form schedules). */
 sk_status sk_tile_block(const sk_gemm_desc* desc, int64_t tile, int64_t* tile_row, int64_t* tile_col);
+/* Co-resident capacity of the persistent kernel for (ab_type, variant) on
+ * `device` (< 0: current): CTAs for the 1-SM and FP64 kernels, CTA pairs for
+ * the 2-SM kernel.  sk_gemm never launches a larger persistent grid, so every
+ * unit a fixup wait points to is resident.  Sets the kernel's per-device
+ * attributes on first use. */
+sk_status sk_persistent_capacity(sk_dtype ab_type, sk_variant variant, int32_t device, int32_t* units);
 /* Stream-ordered, asynchronous.  Does not synchronise. */
 sk_status sk_gemm(const sk_gemm_desc* desc, void* workspace, size_t workspace_bytes,
                   void* stream);

@@ -147,6 +147,7 @@ _SIGS = {
                               C.c_int64, C.c_int64, C.c_void_p, _P(C.c_double), _P(C.c_double),
                               C.c_void_p, C.c_int64, _P(C.c_int64)]),
     "sk_reload_env": (None, []),
+    "sk_persistent_capacity": (C.c_int, [C.c_int, C.c_int, C.c_int32, _P(C.c_int32)]),
 }
 
 
@@ -563,6 +564,16 @@ def load_matrix(path: str, dtype: DType) -> np.ndarray:
         raise MatrixFileError(lib().sk_io_error().decode())
     _check(st, "load_matrix")
     return out
+
+
+def persistent_capacity(ab_type: DType = DType.BFloat16, variant: Variant = Variant.TwoSM,
+                        device: int = -1) -> int:
+    """Co-resident CTAs (CTA pairs for 2-SM) of the persistent kernel on a device:
+    the cap of every launch's persistent grid."""
+    out = C.c_int32()
+    _check(lib().sk_persistent_capacity(int(ab_type), int(variant), device, C.byref(out)),
+           "persistent_capacity")
+    return out.value
 
 
 def reload_env() -> None:

@@ -211,24 +211,60 @@ EncodeTiledFn encode_fn() {
 }
 
 // 2-D row-major tensor: rows x cols elements with leading dimension ld.
+// Encoded maps are cached per host thread (a small ring keyed by every encode
+// argument), so repeated launches on the same buffers skip the driver call.
+struct TmapKey {
+  int dt;
+  size_t esize;
+  const void* base;
+  int64_t rows, cols, ld;
+  uint32_t box_cols, box_rows;
+  int swz, promo;
+  bool operator==(const TmapKey& o) const {
+    return dt == o.dt && esize == o.esize && base == o.base && rows == o.rows && cols == o.cols &&
+           ld == o.ld && box_cols == o.box_cols && box_rows == o.box_rows && swz == o.swz &&
+           promo == o.promo;
+  }
+};
+struct TmapCache {
+  static constexpr int N = 16;
+  TmapKey key[N];
+  CUtensorMap map[N];
+  bool used[N] = {};
+  int next = 0;
+};
+thread_local TmapCache g_tmaps;
+
 sk_status make_tmap(CUtensorMap* m, CUtensorMapDataType dt, size_t esize, const void* base,
                     int64_t rows, int64_t cols, int64_t ld, uint32_t box_cols, uint32_t box_rows,
                     CUtensorMapSwizzle swz) {
+  // 128-B L2 promotion: 8192^3 DP 1468.8 vs 1461.7 (256 B), hybrid 1445.4 vs
+  // 1438.7 TFLOP/s; config 3 and skinny shapes unchanged (profiles/r01/l2_policy.txt).
+  CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+  if (knobs().l2_promo >= 0)  // 0 none, 1 64B, 2 128B, 3 256B
+    promo = static_cast<CUtensorMapL2promotion>(knobs().l2_promo);
+  const TmapKey key{static_cast<int>(dt), esize, base, rows, cols, ld, box_cols, box_rows,
+                    static_cast<int>(swz), static_cast<int>(promo)};
+  TmapCache& c = g_tmaps;
+  for (int i = 0; i < TmapCache::N; ++i)
+    if (c.used[i] && c.key[i] == key) {
+      *m = c.map[i];
+      return SK_OK;
+    }
   EncodeTiledFn fn = encode_fn();
   if (!fn) return fail(SK_ECUDA, "cuTensorMapEncodeTiled unavailable");
   const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
   const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * esize};
   const cuuint32_t box[2] = {box_cols, box_rows};
   const cuuint32_t estr[2] = {1, 1};
-  // 128-B L2 promotion: 8192^3 DP 1468.8 vs 1461.7 (256 B), hybrid 1445.4 vs
-  // 1438.7 TFLOP/s; config 3 and skinny shapes unchanged (profiles/r01/l2_policy.txt).
-  CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
-  if (knobs().l2_promo >= 0)  // 0 none, 1 64B, 2 128B, 3 256B
-    promo = static_cast<CUtensorMapL2promotion>(knobs().l2_promo);
   CUresult r = fn(m, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, swz, promo,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(SK_ECUDA, "cuTensorMapEncodeTiled failed (%d)", int(r));
+  c.key[c.next] = key;
+  c.map[c.next] = *m;
+  c.used[c.next] = true;
+  c.next = (c.next + 1) % TmapCache::N;
   return SK_OK;
 }
 
@@ -831,6 +867,33 @@ sk_status sk_random_matrix(sk_dtype gen_type, int32_t shift, uint64_t seed, int6
 }  // extern "C"
 
 namespace {
+// Co-resident capacity of a persistent kernel on device `dev` (current device):
+// CTAs for the 1-SM and FP64 kernels, CTA pairs for the 2-SM kernel.  Sets the
+// kernel's per-device attributes on first use.
+sk_status resident_units(int dev, const DeviceInfo& info, Kernel kern, int* out) {
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  DeviceInfo& di = g_dev[dev];
+  if (kern == Kernel::F64) {
+    if (!di.f64_ready) {
+      cudaError_t e = f64_max_ctas_per_sm(&di.f64_per_sm);
+      if (e != cudaSuccess) return cuda_fail(e, "sk_gemm_f64 occupancy");
+      if (di.f64_per_sm < 1) return fail(SK_ECUDA, "sk_gemm_f64 does not fit on an SM");
+      di.f64_ready = true;
+    }
+    *out = di.f64_per_sm * info.sms;
+    return SK_OK;
+  }
+  const int cg = kern == Kernel::F16_2SM ? 2 : 1;
+  if (!di.f16_ready[cg]) {
+    cudaError_t e = f16_prepare(cg, info.sms, &di.f16_units[cg]);
+    if (e != cudaSuccess) return cuda_fail(e, "sk_gemm_f16 attributes / occupancy");
+    if (di.f16_units[cg] < 1) return fail(SK_ECUDA, "sk_gemm_f16 does not fit on the device");
+    di.f16_ready[cg] = true;
+  }
+  *out = std::min(di.f16_units[cg], info.sms / cg);
+  return SK_OK;
+}
+
 sk_status gemm_impl(const sk_gemm_desc* d, void* ws, size_t ws_bytes, cudaStream_t strm,
                     const PipeFlags* pipe) {
   const int* a_ready = pipe ? pipe->a_ready : nullptr;
@@ -934,28 +997,8 @@ sk_status gemm_impl(const sk_gemm_desc* d, void* ws, size_t ws_bytes, cudaStream
   // device (queried once per device with the kernel attributes, which are
   // per-device state), so every unit a fixup wait points to is running.
   int resident = 0;
-  {
-    std::lock_guard<std::mutex> lk(g_dev_mu);
-    DeviceInfo& di = g_dev[dev];
-    if (kern == Kernel::F64) {
-      if (!di.f64_ready) {
-        cudaError_t e = f64_max_ctas_per_sm(&di.f64_per_sm);
-        if (e != cudaSuccess) return cuda_fail(e, "sk_gemm_f64 occupancy");
-        if (di.f64_per_sm < 1) return fail(SK_ECUDA, "sk_gemm_f64 does not fit on an SM");
-        di.f64_ready = true;
-      }
-      resident = di.f64_per_sm * info.sms;
-    } else {
-      const int cg = kern == Kernel::F16_2SM ? 2 : 1;
-      if (!di.f16_ready[cg]) {
-        cudaError_t e = f16_prepare(cg, info.sms, &di.f16_units[cg]);
-        if (e != cudaSuccess) return cuda_fail(e, "sk_gemm_f16 attributes / occupancy");
-        if (di.f16_units[cg] < 1) return fail(SK_ECUDA, "sk_gemm_f16 does not fit on the device");
-        di.f16_ready[cg] = true;
-      }
-      resident = std::min(di.f16_units[cg], info.sms / P.ranks);
-    }
-  }
+  st = resident_units(dev, info, kern, &resident);
+  if (st) return st;
   const int64_t units = std::max<int64_t>(s.grid_size, 1);
   const int64_t cap = d->num_ctas > 0 ? d->num_ctas : resident;
   P.num_ctas = std::min<int64_t>(units, std::min<int64_t>(cap, resident));
@@ -1488,6 +1531,30 @@ extern "C" sk_status sk_execute_ranges(const sk_problem* p, const sk_blocking* b
 }
 
 extern "C" void sk_execute_release(void) { g_exec.release(); }
+
+extern "C" sk_status sk_persistent_capacity(sk_dtype ab_type, sk_variant variant, int32_t device,
+                                            int32_t* units) {
+  if (!units) return fail(SK_EINVAL, "null output");
+  sk_gemm_desc d{};
+  d.ab_type = ab_type;
+  d.variant = variant;
+  Kernel k;
+  sk_status st = pick_kernel(&d, &k);
+  if (st) return st;
+  int dev = device;
+  if (dev < 0) SK_CUDA(cudaGetDevice(&dev));
+  int cur = 0;
+  SK_CUDA(cudaGetDevice(&cur));
+  SK_CUDA(cudaSetDevice(dev));
+  DeviceInfo info;
+  st = device_info(dev, &info);
+  int n = 0;
+  if (!st) st = resident_units(dev, info, k, &n);
+  cudaSetDevice(cur);
+  if (st) return st;
+  *units = n;
+  return SK_OK;
+}
 
 extern "C" void sk_reload_env(void) {
   std::lock_guard<std::mutex> lk(g_knob_mu);

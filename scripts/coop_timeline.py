@@ -31,6 +31,7 @@ def main():
     a = sk.stream_k(sk.GemmProblem(m, n, k), blk, args.g)
     for coop in ("0", "1"):
         os.environ["SKB200_COOP"] = coop
+        sk.reload_env()
         g = sk.Gemm(a, sk.DType.BFloat16, sk.Variant.TwoSM, timeline=True)
         for _ in range(10):
             g.run(A, B, C)

@@ -462,6 +462,7 @@ def test_die_aware_lanes_bit_exact(sk, torch_cuda, monkeypatch, var):
         out = []
         for flag in ("0", "1"):
             monkeypatch.setenv("SKB200_DIE_AWARE", flag)
+            sk.reload_env()  # the library reads SKB200_* once
             C = torch.full((m, n), float("nan"), device="cuda")
             gemm = sk.Gemm(a, variant=V)
             gemm.run(A, B, C)
@@ -469,6 +470,8 @@ def test_die_aware_lanes_bit_exact(sk, torch_cuda, monkeypatch, var):
             out.append(C)
         assert torch.equal(out[0], out[1])
         assert torch.equal(out[1].double().sum(1), rows)
+    monkeypatch.undo()
+    sk.reload_env()
 
 
 # ---------------------------------------------------------------- cooperative fixup
@@ -492,6 +495,7 @@ def test_cooperative_fixup_bit_exact(sk, port, torch_cuda, monkeypatch, shape, g
     outs = {}
     for coop in ("1", "0"):
         monkeypatch.setenv("SKB200_COOP", coop)
+        sk.reload_env()
         gemm = sk.Gemm(a, variant=V)
         for name, (X, Y) in (("int", (Ai, Bi)), ("float", (Af, Bf))):
             A = torch.from_numpy(X.astype(np.float32)).cuda().to(torch.bfloat16)
@@ -501,5 +505,7 @@ def test_cooperative_fixup_bit_exact(sk, port, torch_cuda, monkeypatch, shape, g
                 gemm.run(A, B, C)
             gemm.check()
             outs[coop, name] = C.cpu().numpy()
+    monkeypatch.undo()
+    sk.reload_env()
     assert np.array_equal(outs["1", "int"], want)
     assert np.array_equal(outs["1", "float"], outs["0", "float"])

@@ -22,6 +22,7 @@ def pinned(torch, arr):
 def run(sk, a, A, B, compute, variant, pipeline, out):
     old = os.environ.get("SKB200_PIPELINE")
     os.environ["SKB200_PIPELINE"] = "1" if pipeline else "0"
+    sk.reload_env()  # the library reads SKB200_* once
     try:
         out[...] = np.nan
         return sk.execute(a, A, B, compute=compute, variant=variant, out=out).copy()
@@ -30,6 +31,7 @@ def run(sk, a, A, B, compute, variant, pipeline, out):
             del os.environ["SKB200_PIPELINE"]
         else:
             os.environ["SKB200_PIPELINE"] = old
+        sk.reload_env()
 
 
 @pytest.mark.parametrize("var", ["1sm", "2sm", "fp64"])
