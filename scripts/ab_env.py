@@ -4,7 +4,8 @@ settings ROUNDS times on the same box so power/thermal drift hits all arms.
 
   python scripts/ab_env.py --set SKB200_DIE_AWARE=0 --set SKB200_DIE_AWARE=1 \
       [--strategy data_parallel] [--m 8192 --n 8192 --k 8192] [--steps 30 --rounds 4]
-Each --set is one arm: comma-separated VAR=VALUE pairs.
+Each --set is one arm: comma-separated VAR=VALUE pairs (TILE_GROUP=G sets the
+descriptor's tile_group instead of an environment variable).
 """
 import argparse
 import json
@@ -73,7 +74,9 @@ def main():
         for i, env in enumerate(arms):
             for key in {kk for e in arms for kk in e}:  # each arm sets only its own knobs
                 os.environ.pop(key, None)
-            os.environ.update(env)
+            os.environ.update({kk: v for kk, v in env.items() if kk != "TILE_GROUP"})
+            sk.reload_env()  # the library reads SKB200_* once
+            g.desc.tile_group = int(env.get("TILE_GROUP", "0"))  # sk_gemm_desc field, not a knob
             torch.cuda.synchronize()
             time.sleep(args.cool)
             for _ in range(args.warmup):

@@ -177,7 +177,7 @@ def test_trace_ownership_equals_fixup_peers_of(sk, torch_cuda, var):
                 assert tiles[x, 0] == peers[x][0] and tiles[x, 1] == peers[x][-1], (strat, x)
                 assert tiles[x, 2] == peers[x][0]  # stored by the owner
             # every unit whose range starts mid-tile emitted exactly one partial
-            emitted = t[4 * T:]
+            emitted = t[4 * T:4 * T + a.grid_size]
             tbl = a.range_table()
             expect = ((tbl[:, 0] % a.grid.iters_per_tile != 0) & (tbl[:, 1] > tbl[:, 0])).astype(int)
             assert np.array_equal(emitted, expect), strat
