@@ -22,17 +22,24 @@ def main():
     ap.add_argument("--n", type=int, default=1024)
     ap.add_argument("--k", type=int, default=32768)
     ap.add_argument("--g", type=int, default=74)
+    ap.add_argument("--strategy", default="stream_k", choices=["stream_k", "data_parallel", "two_tile_sk_dp"])
+    ap.add_argument("--variant", default="2sm", choices=["1sm", "2sm"])
+    ap.add_argument("--coop", default="0,1")
+    ap.add_argument("--csv", default="", help="write the last timeline (reference CSV format) here")
     args = ap.parse_args()
     m, n, k = args.m, args.n, args.k
     A = (torch.rand(m, k, device="cuda") * 2 - 1).bfloat16()
     B = (torch.rand(k, n, device="cuda") * 2 - 1).bfloat16()
     C = torch.empty(m, n, device="cuda")
-    blk = sk.kernel_blocking(sk.DType.BFloat16, sk.Variant.TwoSM)
-    a = sk.stream_k(sk.GemmProblem(m, n, k), blk, args.g)
-    for coop in ("0", "1"):
+    V = sk.Variant.TwoSM if args.variant == "2sm" else sk.Variant.OneSM
+    blk = sk.kernel_blocking(sk.DType.BFloat16, V)
+    P = sk.GemmProblem(m, n, k)
+    a = {"stream_k": lambda: sk.stream_k(P, blk, args.g), "data_parallel": lambda: sk.data_parallel(P, blk),
+         "two_tile_sk_dp": lambda: sk.hybrid(P, blk, args.g, sk.HybridVariant.TwoTileSkDp)}[args.strategy]()
+    for coop in args.coop.split(","):
         os.environ["SKB200_COOP"] = coop
         sk.reload_env()
-        g = sk.Gemm(a, sk.DType.BFloat16, sk.Variant.TwoSM, timeline=True)
+        g = sk.Gemm(a, sk.DType.BFloat16, V, timeline=True)
         for _ in range(10):
             g.run(A, B, C)
         torch.cuda.synchronize()
@@ -47,7 +54,13 @@ def main():
                "partial_done_us": [float(np.median(us(r[part, 7]))), float(us(r[part, 7].max()))] if part.any() else None,
                "owner_wait_end_us": [float(np.median(us(r[own, 6]))), float(us(r[own, 6].max()))] if own.any() else None,
                "owner_done_us": [float(np.median(us(r[own, 7]))), float(us(r[own, 7].max()))] if own.any() else None}
+        out.update(shape=[m, n, k], strategy=args.strategy, g=a.grid_size, variant=args.variant)
         print(json.dumps(out))
+        if args.csv:
+            from paper_2301_03598_b200 import timeline as tlm
+
+            with open(args.csv, "w") as f:
+                tlm.write_timeline_csv(tlm.from_device(r), f)
 
 
 if __name__ == "__main__":

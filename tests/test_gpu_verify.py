@@ -111,7 +111,7 @@ def test_trace_blocks_follow_row_major_map(sk, torch_cuda, var):
     V = sk.Variant.OneSM if var == "1sm" else sk.Variant.TwoSM
     p = 148 if var == "1sm" else 74
     blk = sk.kernel_blocking(sk.DType.BFloat16, V)
-    for shape in ((8192, 8192, 1024), (1280, 3840, 512), (2304, 2304, 2048), (1000, 3000, 700)):
+    for shape in ((8192, 8192, 1024), (1280, 3840, 512), (2304, 2304, 2048), (1000, 3008, 704)):
         P = sk.GemmProblem(*shape)
         A = torch.zeros(P.m, P.k, dtype=torch.bfloat16, device="cuda")
         B = torch.zeros(P.k, P.n, dtype=torch.bfloat16, device="cuda")
