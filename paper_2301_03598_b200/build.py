@@ -43,11 +43,15 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: str = "") -> str:
+    """Build libskb200.so; `out` (or $SKB200_LIB_OUT) writes an experimental
+    variant elsewhere (loaded with $SKB200_LIB) instead of the product library."""
+    out = out or os.environ.get("SKB200_LIB_OUT", "")
+    lib = out or LIB
+    if not out and not force and not _stale():
         return LIB
-    os.makedirs(LIBDIR, exist_ok=True)
-    tmp = LIB + ".tmp"
+    os.makedirs(os.path.dirname(lib), exist_ok=True)
+    tmp = lib + ".tmp"
     cmd = [
         nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared",
         "-Xcompiler", "-fPIC", "-Xptxas", "-v" if verbose else "-O3",
@@ -65,8 +69,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError("nvcc build of libskb200.so failed")
     if verbose:
         sys.stderr.write(res.stderr)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":

@@ -142,6 +142,21 @@ __device__ __forceinline__ void mbar_arrive_remote(uint32_t bar_cluster_addr) {
                : "memory");
 }
 
+// Epilogue probe (experiments only, -DSKB200_EPI_PROBE): per (CTA, epilogue
+// warp) globaltimer stamps of the warp's last segment in cta_clocks[16 * slot].
+#ifdef SKB200_EPI_PROBE
+#define EPI_STAMP(slot)                                                                              \
+  do {                                                                                               \
+    if (P.cta_clocks && lane == 0)                                                                   \
+      P.cta_clocks[(static_cast<int64_t>(blockIdx.x) * EPI_WARPS + (warp - 2)) * 16 + (slot)] =      \
+          static_cast<long long>(ptx::globaltimer());                                                \
+  } while (0)
+#else
+#define EPI_STAMP(slot) \
+  do {                  \
+  } while (0)
+#endif
+
 template <int CG>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     sk_gemm_f16(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -204,7 +219,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   // kernel's tail; nothing below touches global memory before it completes.
   ptx::grid_dependency_wait();
   ptx::launch_dependents();
+#ifndef SKB200_EPI_PROBE
   stamp_clock(P, 0);
+#endif
 
   if (warp == 0) {
     // ===================== TMA producer (every CTA of the pair) =====================
@@ -432,6 +449,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                      [&](int64_t u, int64_t tile, int64_t lb, int64_t le) {
       ptx::mbar_wait(&tfull_bar[acc], acc_phase);
       ptx::tc_fence_after();
+      EPI_STAMP(0);
       long long* ev = (leader && rank == 0) ? event_slot(P, u, tile) : nullptr;
       if (ev) ev[kEvMacEnd] = ptx::globaltimer();
       const uint32_t tsrc = tmem_base + acc * BN + ((q * 32) << 16);
@@ -453,6 +471,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         __syncwarp();
       }
       if (ev) ev[kEvWaitEnd] = ptx::globaltimer();
+      EPI_STAMP(15);
       const int64_t my_idx = partial ? fidx(u) : own_base + fidx(u);
       float* my_slab = publish ? slab(my_idx) : nullptr;
       // 64 columns (two 32-column chunks) per step: one tcgen05.ld.x64, 16 float4
@@ -467,6 +486,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (int c = c_lo; c < c_end; c += 2) {
         float v[64];
         ptx::tmem_ld64(tsrc + c * 32, v);
+        EPI_STAMP(1 + 3 * ((c - c_lo) / 2 % 4));
         if (publish) {
 #pragma unroll
           for (int j = 0; j < 16; ++j)
@@ -490,14 +510,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             // The slab lines this warp just consumed are dead: drop them from L2
             // without a DRAM write-back (one lane per 128-B line).
             __syncwarp();
+#ifndef SKB200_NO_DISCARD
             if ((lane & 7) == 0) {
 #pragma unroll
               for (int j = 0; j < 16; ++j) ptx::discard_l2(slab_ptr(ps, c + j / 8, j % 8, row));
             }
+#endif
           }
+          EPI_STAMP(2 + 3 * ((c - c_lo) / 2 % 4));
           store_box(v, n0, m0, c);
           store_box(v + 32, n0, m0, c + 1);
         }
+        EPI_STAMP(3 + 3 * ((c - c_lo) / 2 % 4));
       }
       // Accumulator drained: hand the TMEM buffer back to the (leader's) MMA warp.
       ptx::tc_fence_before();
@@ -514,6 +538,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (P.trace && rank == 0 && partial) atomicAdd(P.trace + 4 * s.total_tiles + u, 1);
         }
       }
+      EPI_STAMP(13);
       if (!partial) {
         if (P.c_done) {  // this warp's rows of the tile are in HBM: count them for copy-out
           if (lane == 0) {
@@ -566,6 +591,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }, P.sk_first, P.dp_perm);
     if (lane == 0) ptx::tma_store_wait_all<0>();
     __syncwarp();
+    EPI_STAMP(14);
   }
 
   ptx::tc_fence_before();
@@ -573,7 +599,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if constexpr (CG == 2) cluster_sync();  // the leader's MMAs touch the peer's smem/TMEM
   ptx::tc_fence_after();
   if (warp == 1) ptx::tmem_dealloc<CG>(tmem_base, TMEM_COLS);
+#ifndef SKB200_EPI_PROBE
   stamp_clock(P, 1);
+#endif
 #endif
 }
 

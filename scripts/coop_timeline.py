@@ -28,9 +28,9 @@ def main():
     ap.add_argument("--csv", default="", help="write the last timeline (reference CSV format) here")
     args = ap.parse_args()
     m, n, k = args.m, args.n, args.k
-    A = (torch.rand(m, k, device="cuda") * 2 - 1).bfloat16()
-    B = (torch.rand(k, n, device="cuda") * 2 - 1).bfloat16()
-    C = torch.empty(m, n, device="cuda")
+    A = sk.random_matrix_device(m, k, 42, sk.DType.Float32, sk.DType.BFloat16)  # 16-byte rows
+    B = sk.random_matrix_device(k, n, 43, sk.DType.Float32, sk.DType.BFloat16)
+    C = torch.empty(m, -(-n // 4) * 4, device="cuda")[:, :n]
     V = sk.Variant.TwoSM if args.variant == "2sm" else sk.Variant.OneSM
     blk = sk.kernel_blocking(sk.DType.BFloat16, V)
     P = sk.GemmProblem(m, n, k)

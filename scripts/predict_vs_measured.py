@@ -1,0 +1,135 @@
+"""Row f4 of SURVEY.md section 8(f): the reference simulator fed with cost
+constants calibrated from this kernel's own device timelines, predicted vs
+measured makespan.
+
+  python scripts/predict_vs_measured.py --out profiles/r02/predict_vs_measured.json
+
+For every (shape, strategy) the kernel runs with per-segment %globaltimer
+stamps (Gemm(..., timeline=True)).  Per logical unit (the reference's CTA):
+  mac     = last segment's mainloop end - first segment's mainloop start,
+  reduce  = sum over its owner-with-peers segments of (done - wait end).
+Calibration (least squares, non-negative) fits the reference's CostParams
+(costmodel.hpp:13-19, simulate.cpp:43-62):  mac = a + c * len + b * [partial],
+reduce = d * peers, on the calibration shapes; then simulate(assignment, p,
+params) (the library's restatement of simulate.cpp:23-69) predicts each
+launch's makespan, compared with the measured one (last epilogue end - first
+mainloop start).  The unit-cost simulation is reported beside it.
+"""
+import argparse
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2301_03598_b200 as sk  # noqa: E402
+
+CAL = [(1024, 1024, 8192), (2048, 2048, 2048), (1280, 3840, 4096), (4096, 4096, 1024),
+       (768, 768, 16384), (3072, 3072, 3072)]
+EVAL = [(1024, 1024, 32768), (1024, 4864, 4096), (2560, 3840, 4096), (8192, 8192, 8192),
+        (2304, 2304, 8192), (583, 1906, 4544), (128, 8192, 8192), (4096, 4096, 4096)]
+
+
+def measure(a, V, reps=5):
+    m, n, k = a.problem.m, a.problem.n, a.problem.k
+    A = sk.random_matrix_device(m, k, 42, sk.DType.Float32, sk.DType.BFloat16)
+    B = sk.random_matrix_device(k, n, 43, sk.DType.Float32, sk.DType.BFloat16)
+    al = 4
+    C = torch.empty(m, -(-n // al) * al, device="cuda")[:, :n]
+    plain = sk.Gemm(a, sk.DType.BFloat16, V)
+    g = sk.Gemm(a, sk.DType.BFloat16, V, timeline=True)
+    for _ in range(reps):
+        plain.run(A, B, C)
+    g.run(A, B, C)
+    torch.cuda.synchronize()
+    g.check()
+    return g.timeline()
+
+
+def per_unit(rec, a):
+    """{unit: (len, partial, mac_us, reduce_us, peers)} from the device records."""
+    ipt = a.grid.iters_per_tile
+    tbl = a.range_table()
+    peers = sk.fixup_peers_of(a)
+    out = {}
+    for u in np.unique(rec[:, 0]):
+        r = rec[rec[:, 0] == u]
+        b, e = tbl[int(u)]
+        mac = (r[:, 5].max() - r[:, 4].min()) * 1e-3
+        own = r[(r[:, 3] & 2) != 0]
+        red = float(((own[:, 7] - own[:, 6]) * 1e-3).sum()) if len(own) else 0.0
+        npeer = sum(len(p) - 1 for p in peers if len(p) > 1 and p[0] == u)
+        out[int(u)] = (int(e - b), int(b % ipt != 0), float(mac), red, npeer)
+    return out
+
+
+def nnls(X, y):
+    from scipy.optimize import nnls as _nnls
+
+    return _nnls(X, y)[0]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", default="")
+    ap.add_argument("--variant", default="2sm")
+    args = ap.parse_args()
+    V = sk.Variant.TwoSM if args.variant == "2sm" else sk.Variant.OneSM
+    p = 74 if args.variant == "2sm" else 148
+    blk = sk.kernel_blocking(sk.DType.BFloat16, V)
+
+    def cases(shapes):
+        for shp in shapes:
+            P = sk.GemmProblem(*shp)
+            for a in (sk.data_parallel(P, blk), sk.stream_k(P, blk, p),
+                      sk.hybrid(P, blk, p, sk.HybridVariant.TwoTileSkDp)):
+                yield shp, a
+
+    runs = {}
+    for shp, a in list(cases(CAL)) + list(cases(EVAL)):
+        rec = measure(a, V)
+        runs[(shp, sk.strategy_name(a.strategy))] = (a, rec)
+    # ---- calibrate on CAL
+    Xm, ym, xr, yr = [], [], [], []
+    for shp in CAL:
+        for name in ("data_parallel", "stream_k", "two_tile_sk_dp"):
+            a, rec = runs[(shp, name)]
+            for ln, part, mac, red, npeer in per_unit(rec, a).values():
+                Xm.append([1.0, float(part), float(ln)])
+                ym.append(mac)
+                if npeer:
+                    xr.append(float(npeer))
+                    yr.append(red)
+    a_, b_, c_ = nnls(np.array(Xm), np.array(ym))
+    d_ = float(np.dot(xr, yr) / np.dot(xr, xr)) if xr else 0.0
+    params = {"a": float(a_), "b": float(b_), "c": float(c_), "d": d_}
+    rows = []
+    for (shp, name), (a, rec) in runs.items():
+        measured = float((rec[:, 7].max() - rec[:, 4].min()) * 1e-3)
+        pred, util = sk.simulate(a, p, params)
+        unit_ms, unit_util = sk.simulate(a, p)
+        rows.append({"shape": list(shp), "strategy": name, "g": a.grid_size,
+                     "set": "calibration" if shp in CAL else "evaluation",
+                     "measured_us": round(measured, 2), "predicted_us": round(pred, 2),
+                     "rel_err": round((pred - measured) / measured, 4),
+                     "predicted_utilization": round(util, 4),
+                     "unit_cost_makespan_iters": unit_ms, "unit_cost_utilization": round(unit_util, 4)})
+        print(json.dumps(rows[-1]), flush=True)
+    ev = [abs(r["rel_err"]) for r in rows if r["set"] == "evaluation"]
+    summary = {"params_us": params, "p": p, "variant": args.variant,
+               "fit": "mac = a + c*len + b*[partial], reduce = d*peers (simulate.cpp:43-62), NNLS on "
+                      "calibration shapes' device timelines",
+               "eval_median_abs_rel_err": float(np.median(ev)), "eval_max_abs_rel_err": float(max(ev)),
+               "rows": rows}
+    print(json.dumps({k: v for k, v in summary.items() if k != "rows"}))
+    if args.out:
+        os.makedirs(os.path.dirname(args.out), exist_ok=True)
+        with open(args.out, "w") as f:
+            json.dump(summary, f, indent=1)
+
+
+if __name__ == "__main__":
+    main()
