@@ -67,6 +67,11 @@ constexpr int UMMA_K = 16;
 #define SKB200_EPI_BUFS (SKB200_EPI_WARPS == 8 ? 1 : 2)
 #endif
 constexpr int EPI_WARPS = SKB200_EPI_WARPS;
+// Owner-fold slab loads in flight per epilogue warp (jobs of 32 columns x one
+// peer): 0 = one peer batch of 64 columns per round trip.
+#ifndef SKB200_FOLD_RING
+#define SKB200_FOLD_RING 0
+#endif
 static_assert(EPI_WARPS == 4 || EPI_WARPS == 8, "4 or 8 epilogue warps");
 constexpr int EPI_COLS = BN / (EPI_WARPS / 4);  // accumulator columns per epilogue warp
 constexpr int EPI_BUFS = SKB200_EPI_BUFS;   // 4-KB TMA-store staging boxes per epilogue warp
@@ -482,46 +487,116 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const int c_end = (orphan || m0 + static_cast<int32_t>(q * 32) >= s.m)
                             ? c_lo
                             : imin(c_lo + EPI_COLS / 32, 2 * ceil_div(s.n - n0, 64));
-#pragma unroll 1
-      for (int c = c_lo; c < c_end; c += 2) {
-        float v[64];
-        ptx::tmem_ld64(tsrc + c * 32, v);
-        EPI_STAMP(1 + 3 * ((c - c_lo) / 2 % 4));
-        if (publish) {
+#if SKB200_FOLD_RING > 0
+      if (fold_n > 0) {
+        // Owner fold, software-pipelined (executor.hpp:165-172 order: own
+        // accumulator, then peers in ascending id).  The fold is a sequence of
+        // (32-column chunk, peer) jobs of 4 KB per warp; SKB200_FOLD_RING jobs'
+        // slab loads are in flight at any time (register buffers in an unrolled
+        // ring), so the L2 round trips of consecutive peers and chunks overlap
+        // instead of serialising one batch per round trip.
+        const int jobs = (c_end - c_lo) * fold_n;
+        float4 b0[8], b1[8];
+#if SKB200_FOLD_RING > 2
+        float4 b2[8];
+#endif
+        float v[32];
+        auto issue = [&](int j, float4 (&b)[8]) {
+          if (j < jobs) {
+            const int ch = c_lo + j / fold_n;
+            float* ps = slab(fidx(s.peer(tile, u, 1 + j % fold_n)));
 #pragma unroll
-          for (int j = 0; j < 16; ++j)
-            ptx::st_cg_f4(slab_ptr(my_slab, c + j / 8, j % 8, row),
-                          make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
-        } else {
-          // Owner fold: own accumulator, then peers in ascending id (executor.hpp:165-172).
-#pragma unroll 1
-          for (int p = 1; p <= fold_n; ++p) {
-            float* ps = slab(fidx(s.peer(tile, u, p)));
-            float4 w[16];
+            for (int i = 0; i < 8; ++i) b[i] = ptx::ld_cg_f4(slab_ptr(ps, ch, i, row));
+          }
+        };
+        auto consume = [&](int j, float4 (&b)[8]) {
+          if (j >= jobs) return;
+          const int ch = c_lo + j / fold_n, pp = j % fold_n;
+          if (pp == 0) ptx::tmem_ld32(tsrc + ch * 32, v);
 #pragma unroll
-            for (int j = 0; j < 16; ++j) w[j] = ptx::ld_cg_f4(slab_ptr(ps, c + j / 8, j % 8, row));
-#pragma unroll
-            for (int j = 0; j < 16; ++j) {
-              v[4 * j] += w[j].x;
-              v[4 * j + 1] += w[j].y;
-              v[4 * j + 2] += w[j].z;
-              v[4 * j + 3] += w[j].w;
-            }
-            // The slab lines this warp just consumed are dead: drop them from L2
-            // without a DRAM write-back (one lane per 128-B line).
+          for (int i = 0; i < 8; ++i) {
+            v[4 * i] += b[i].x;
+            v[4 * i + 1] += b[i].y;
+            v[4 * i + 2] += b[i].z;
+            v[4 * i + 3] += b[i].w;
+          }
+          issue(j + SKB200_FOLD_RING, b);
+          if (pp == fold_n - 1) {
+            // Every lane has consumed the chunk from every peer: its slab lines
+            // are dead, drop them from L2 without a DRAM write-back (lane l:
+            // 128-B line l of the warp's 4 KB).
             __syncwarp();
 #ifndef SKB200_NO_DISCARD
-            if ((lane & 7) == 0) {
-#pragma unroll
-              for (int j = 0; j < 16; ++j) ptx::discard_l2(slab_ptr(ps, c + j / 8, j % 8, row));
-            }
+            for (int p = 1; p <= fold_n; ++p)
+              ptx::discard_l2(reinterpret_cast<const char*>(
+                                  slab_ptr(slab(fidx(s.peer(tile, u, p))), ch, lane / 4, q * 32)) +
+                              (lane % 4) * 128);
 #endif
+            store_box(v, n0, m0, ch);
           }
-          EPI_STAMP(2 + 3 * ((c - c_lo) / 2 % 4));
-          store_box(v, n0, m0, c);
-          store_box(v + 32, n0, m0, c + 1);
+        };
+        issue(0, b0);
+        issue(1, b1);
+#if SKB200_FOLD_RING > 2
+        issue(2, b2);
+#endif
+        EPI_STAMP(1);
+#pragma unroll 1
+        for (int j = 0; j < jobs; j += SKB200_FOLD_RING) {
+          consume(j, b0);
+          consume(j + 1, b1);
+#if SKB200_FOLD_RING > 2
+          consume(j + 2, b2);
+#endif
         }
-        EPI_STAMP(3 + 3 * ((c - c_lo) / 2 % 4));
+        EPI_STAMP(2);
+        EPI_STAMP(3);
+      } else
+#endif  // SKB200_FOLD_RING
+      {
+#pragma unroll 1
+        for (int c = c_lo; c < c_end; c += 2) {
+          float v[64];
+          ptx::tmem_ld64(tsrc + c * 32, v);
+          EPI_STAMP(1 + 3 * ((c - c_lo) / 2 % 4));
+          if (publish) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              ptx::st_cg_f4(slab_ptr(my_slab, c + j / 8, j % 8, row),
+                            make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
+            EPI_STAMP(2 + 3 * ((c - c_lo) / 2 % 4));
+          } else {
+            // Owner fold, one peer batch per round trip: own accumulator, then
+            // peers in ascending id (executor.hpp:165-172).
+#pragma unroll 1
+            for (int p = 1; p <= fold_n; ++p) {
+              float* ps = slab(fidx(s.peer(tile, u, p)));
+              float4 w[16];
+#pragma unroll
+              for (int j = 0; j < 16; ++j) w[j] = ptx::ld_cg_f4(slab_ptr(ps, c + j / 8, j % 8, row));
+#pragma unroll
+              for (int j = 0; j < 16; ++j) {
+                v[4 * j] += w[j].x;
+                v[4 * j + 1] += w[j].y;
+                v[4 * j + 2] += w[j].z;
+                v[4 * j + 3] += w[j].w;
+              }
+              // The slab lines this warp just consumed are dead: drop them from L2
+              // without a DRAM write-back (one lane per 128-B line).
+              __syncwarp();
+#ifndef SKB200_NO_DISCARD
+              if ((lane & 7) == 0) {
+#pragma unroll
+                for (int j = 0; j < 16; ++j) ptx::discard_l2(slab_ptr(ps, c + j / 8, j % 8, row));
+              }
+#endif
+            }
+            EPI_STAMP(2 + 3 * ((c - c_lo) / 2 % 4));
+            store_box(v, n0, m0, c);
+            store_box(v + 32, n0, m0, c + 1);
+          }
+          EPI_STAMP(3 + 3 * ((c - c_lo) / 2 % 4));
+        }
       }
       // Accumulator drained: hand the TMEM buffer back to the (leader's) MMA warp.
       ptx::tc_fence_before();

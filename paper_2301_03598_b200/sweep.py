@@ -430,7 +430,8 @@ def write_csv(path, rows):
 
 def main(argv=None):
     ap = argparse.ArgumentParser()
-    ap.add_argument("--shapes", default="config3", choices=["config3", "config4", "corpus", "skinny"])
+    ap.add_argument("--shapes", default="config3",
+                    help="config3 | config4 | corpus | skinny | file:<path> (lines m,n,k[,seed])")
     ap.add_argument("--count", type=int, default=32824)
     ap.add_argument("--offset", type=int, default=0)
     ap.add_argument("--lo", type=int, default=128)
@@ -462,10 +463,17 @@ def main(argv=None):
         shapes = CONFIG4
     elif args.shapes == "skinny":
         shapes = SKINNY
-    else:
+    elif args.shapes.startswith("file:"):
+        with open(args.shapes[5:]) as f:
+            recs = [[int(x) for x in line.split(",")] for line in f if line.strip() and line[0].isdigit()]
+        shapes = [tuple(r[:3]) for r in recs]
+        seeds = [r[3] if len(r) > 3 else 42 for r in recs]
+    elif args.shapes == "corpus":
         c = sk.corpus(args.seed, args.offset + args.count, args.lo, args.hi)[args.offset:]
         shapes = [tuple(int(x) for x in r[:3]) for r in c]
         seeds = [int(r[3]) for r in c]  # run_sweep's per-shape matrix_seed (sweep.cpp:86)
+    else:
+        raise SystemExit(f"unknown --shapes {args.shapes}")
     names = args.strategies.split(",")
     variant = sk.Variant.TwoSM if args.variant == "2sm" else sk.Variant.OneSM
     force_full = args.cpu_full == "all" or (args.cpu_full == "auto" and args.shapes != "corpus")
