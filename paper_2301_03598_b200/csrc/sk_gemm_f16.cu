@@ -67,11 +67,13 @@ constexpr int UMMA_K = 16;
 #define SKB200_EPI_BUFS (SKB200_EPI_WARPS == 8 ? 1 : 2)
 #endif
 constexpr int EPI_WARPS = SKB200_EPI_WARPS;
-// Owner-fold slab loads in flight per epilogue warp (jobs of 32 columns x one
-// peer): 0 = one peer batch of 64 columns per round trip.
-#ifndef SKB200_FOLD_RING
-#define SKB200_FOLD_RING 0
-#endif
+// -DSKB200_DISCARD: drop consumed fixup-slab lines from L2 (discard.global.L2)
+// instead of letting them age out.  Off: the discards sit on the owner's fold
+// path and cost more than the write-backs they save -- Stream-K picks on the
+// 225 near-regression corpus shapes 1.006x -> 1.024x of DP, 9 -> 0 shapes more
+// than 5 % slower, config 3 1.40 -> 1.42, 8192^3 unchanged
+// (profiles/r02/discard_ab.txt).
+
 static_assert(EPI_WARPS == 4 || EPI_WARPS == 8, "4 or 8 epilogue warps");
 constexpr int EPI_COLS = BN / (EPI_WARPS / 4);  // accumulator columns per epilogue warp
 constexpr int EPI_BUFS = SKB200_EPI_BUFS;   // 4-KB TMA-store staging boxes per epilogue warp
@@ -425,6 +427,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               a[j].x += w0[j].x; a[j].y += w0[j].y; a[j].z += w0[j].z; a[j].w += w0[j].w;
             }
           }
+#ifdef SKB200_DISCARD
           // Every lane has consumed the chunk: its slab lines are dead, drop them
           // from L2 without a write-back (lane l: line l of the warp's 4 KB).
           __syncwarp();
@@ -433,6 +436,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           for (int64_t pd = owner + 1; pd <= last; ++pd)
             ptx::discard_l2(reinterpret_cast<const char*>(slab_ptr(slab(fidx(pd)), c, lane / 4, q * 32)) +
                             (lane % 4) * 128);
+#endif
           store_box(reinterpret_cast<const float*>(a), n0, m0, c);
         }
       }
@@ -487,72 +491,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const int c_end = (orphan || m0 + static_cast<int32_t>(q * 32) >= s.m)
                             ? c_lo
                             : imin(c_lo + EPI_COLS / 32, 2 * ceil_div(s.n - n0, 64));
-#if SKB200_FOLD_RING > 0
-      if (fold_n > 0) {
-        // Owner fold, software-pipelined (executor.hpp:165-172 order: own
-        // accumulator, then peers in ascending id).  The fold is a sequence of
-        // (32-column chunk, peer) jobs of 4 KB per warp; SKB200_FOLD_RING jobs'
-        // slab loads are in flight at any time (register buffers in an unrolled
-        // ring), so the L2 round trips of consecutive peers and chunks overlap
-        // instead of serialising one batch per round trip.
-        const int jobs = (c_end - c_lo) * fold_n;
-        float4 b0[8], b1[8];
-#if SKB200_FOLD_RING > 2
-        float4 b2[8];
-#endif
-        float v[32];
-        auto issue = [&](int j, float4 (&b)[8]) {
-          if (j < jobs) {
-            const int ch = c_lo + j / fold_n;
-            float* ps = slab(fidx(s.peer(tile, u, 1 + j % fold_n)));
-#pragma unroll
-            for (int i = 0; i < 8; ++i) b[i] = ptx::ld_cg_f4(slab_ptr(ps, ch, i, row));
-          }
-        };
-        auto consume = [&](int j, float4 (&b)[8]) {
-          if (j >= jobs) return;
-          const int ch = c_lo + j / fold_n, pp = j % fold_n;
-          if (pp == 0) ptx::tmem_ld32(tsrc + ch * 32, v);
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            v[4 * i] += b[i].x;
-            v[4 * i + 1] += b[i].y;
-            v[4 * i + 2] += b[i].z;
-            v[4 * i + 3] += b[i].w;
-          }
-          issue(j + SKB200_FOLD_RING, b);
-          if (pp == fold_n - 1) {
-            // Every lane has consumed the chunk from every peer: its slab lines
-            // are dead, drop them from L2 without a DRAM write-back (lane l:
-            // 128-B line l of the warp's 4 KB).
-            __syncwarp();
-#ifndef SKB200_NO_DISCARD
-            for (int p = 1; p <= fold_n; ++p)
-              ptx::discard_l2(reinterpret_cast<const char*>(
-                                  slab_ptr(slab(fidx(s.peer(tile, u, p))), ch, lane / 4, q * 32)) +
-                              (lane % 4) * 128);
-#endif
-            store_box(v, n0, m0, ch);
-          }
-        };
-        issue(0, b0);
-        issue(1, b1);
-#if SKB200_FOLD_RING > 2
-        issue(2, b2);
-#endif
-        EPI_STAMP(1);
-#pragma unroll 1
-        for (int j = 0; j < jobs; j += SKB200_FOLD_RING) {
-          consume(j, b0);
-          consume(j + 1, b1);
-#if SKB200_FOLD_RING > 2
-          consume(j + 2, b2);
-#endif
-        }
-        EPI_STAMP(2);
-        EPI_STAMP(3);
-      } else
-#endif  // SKB200_FOLD_RING
       {
 #pragma unroll 1
         for (int c = c_lo; c < c_end; c += 2) {
@@ -584,7 +522,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               // The slab lines this warp just consumed are dead: drop them from L2
               // without a DRAM write-back (one lane per 128-B line).
               __syncwarp();
-#ifndef SKB200_NO_DISCARD
+#ifdef SKB200_DISCARD
               if ((lane & 7) == 0) {
 #pragma unroll
                 for (int j = 0; j < 16; ++j) ptx::discard_l2(slab_ptr(ps, c + j / 8, j % 8, row));
