@@ -101,7 +101,10 @@ struct Cfg {
   static constexpr int b_off = a_off + STAGES * A_STAGE;
   static constexpr int epi_off = b_off + STAGES * B_STAGE;
   static constexpr int bar_off = epi_off + EPI_BYTES;
-  static constexpr int bar_bytes = (2 * STAGES + 4) * 8 + 16;
+  static constexpr int bar_bytes = (2 * STAGES + 6) * 8 + 16;
+  // Tail fold: the ring's bytes hold 16 KB chunks of peer slabs, two batches.
+  static constexpr int TAIL_SLOT = ROWS * 32 * 4;
+  static constexpr int TAIL_BATCH = epi_off / TAIL_SLOT / 2;
   static constexpr int alloc = bar_off + bar_bytes + 1024;  // + runtime 1 KB alignment
   static_assert(alloc <= 232448, "smem budget");
 };
@@ -180,7 +183,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* empty_bar = full_bar + K::STAGES;
   uint64_t* tfull_bar = empty_bar + K::STAGES;
   uint64_t* tempty_bar = tfull_bar + 2;
-  uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  uint64_t* tail_bar = tempty_bar + 2;
+  uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(tail_bar + 2);
   int* lane_code_smem = reinterpret_cast<int*>(tmem_base_smem + 1);
 
   const uint32_t warp = threadIdx.x / 32;
@@ -201,6 +205,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&tfull_bar[i], 1);
       ptx::mbar_init(&tempty_bar[i], EPI_WARPS * CG);
+      ptx::mbar_init(&tail_bar[i], 1);
     }
     ptx::fence_barrier_init();
     // Die-aware DP lane (die_lane): keyed by the leader CTA's SM, shared with the peer.
@@ -454,8 +459,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     };
     int64_t pend0 = 0, pend1 = 0;  // this unit's published shared tiles (at most two)
     int npend = 0;
-    for_each_segment(s, cta, P.num_ctas, dp_lane, P.raster_rows,
-                     [&](int64_t u, int64_t tile, int64_t lb, int64_t le) {
+    // final_seg: the CTA's last segment -- its mainloop has drained the smem
+    // ring, which the tail fold below reuses.
+    auto segment = [&](int64_t u, int64_t tile, int64_t lb, int64_t le, bool final_seg) {
       ptx::mbar_wait(&tfull_bar[acc], acc_phase);
       ptx::tc_fence_after();
       EPI_STAMP(0);
@@ -474,10 +480,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const bool coop_t = P.coop && (partial || npeer > 0);
       const bool publish = partial || coop_t;
       const int fold_n = coop_t ? 0 : npeer;  // peers this owner folds itself
+      // Tail fold: on the CTA's final segment the owner streams its peers' slabs
+      // into the (now idle) smem ring with bulk copies -- the TMA engine keeps
+      // 96 KB of slab reads in flight instead of the epilogue warps' 32 KB of
+      // register loads -- and the warps fold them from smem (same order).
+      const bool tail = EPI_WARPS == 4 && final_seg && fold_n > 0;
       if (fold_n > 0) {
-        if (lane == 0)
-          for (int p = 1; p <= fold_n; ++p) wait_flag(P, P.flags + fidx(s.peer(tile, u, p)));
-        __syncwarp();
+        if (tail) {
+          if (leader) {
+            for (int p = 1; p <= fold_n; ++p) wait_flag(P, P.flags + fidx(s.peer(tile, u, p)));
+            ptx::fence_proxy_async_global();  // peers' generic-proxy slab writes -> bulk reads
+          }
+        } else {
+          if (lane == 0)
+            for (int p = 1; p <= fold_n; ++p) wait_flag(P, P.flags + fidx(s.peer(tile, u, p)));
+          __syncwarp();
+        }
       }
       if (ev) ev[kEvWaitEnd] = ptx::globaltimer();
       EPI_STAMP(15);
@@ -491,7 +509,55 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const int c_end = (orphan || m0 + static_cast<int32_t>(q * 32) >= s.m)
                             ? c_lo
                             : imin(c_lo + EPI_COLS / 32, 2 * ceil_div(s.n - n0, 64));
-      {
+      if (tail) {
+        // jobs j = (chunk j / fold_n, peer 1 + j % fold_n), chunk-major: each
+        // chunk's peers are folded in ascending id (executor.hpp:165-172).
+        const int nch = m0 >= s.m ? 0 : imin(EPI_COLS / 32, 2 * ceil_div(s.n - n0, 64));
+        const int J = nch * fold_n, NB = (J + K::TAIL_BATCH - 1) / K::TAIL_BATCH;
+        auto issue = [&](int b) {
+          if (!leader || b >= NB) return;
+          const int j0 = b * K::TAIL_BATCH, nj = imin(K::TAIL_BATCH, J - j0);
+          uint64_t* bar = &tail_bar[b & 1];
+          ptx::fence_proxy_async_smem();  // generic reads of the slots precede the refill
+          ptx::mbar_expect_tx(bar, static_cast<uint32_t>(nj * K::TAIL_SLOT));
+          for (int i = 0; i < nj; ++i) {
+            const int j = j0 + i;
+            const float* src = slab(fidx(s.peer(tile, u, 1 + j % fold_n))) + (j / fold_n) * (K::TAIL_SLOT / 4);
+            ptx::bulk_load(smem + ((b & 1) * K::TAIL_BATCH + i) * K::TAIL_SLOT, src, K::TAIL_SLOT, bar);
+          }
+        };
+        issue(0);
+        issue(1);
+        EPI_STAMP(1);
+        float v[32];
+#pragma unroll 1
+        for (int b = 0; b < NB; ++b) {
+          const int j0 = b * K::TAIL_BATCH, nj = imin(K::TAIL_BATCH, J - j0);
+          if (c_end > c_lo) {
+            ptx::mbar_wait(&tail_bar[b & 1], (b >> 1) & 1);
+#pragma unroll 1
+            for (int i = 0; i < nj; ++i) {
+              const int j = j0 + i, ch = j / fold_n, pp = j % fold_n;
+              if (pp == 0) ptx::tmem_ld32(tsrc + ch * 32, v);
+              const float4* sl =
+                  reinterpret_cast<const float4*>(smem + ((b & 1) * K::TAIL_BATCH + i) * K::TAIL_SLOT);
+#pragma unroll
+              for (int jj = 0; jj < 8; ++jj) {
+                const float4 w = sl[jj * ROWS + row];
+                v[4 * jj] += w.x;
+                v[4 * jj + 1] += w.y;
+                v[4 * jj + 2] += w.z;
+                v[4 * jj + 3] += w.w;
+              }
+              if (pp == fold_n - 1) store_box(v, n0, m0, ch);
+            }
+          }
+          ptx::named_bar_sync(1, 32 * EPI_WARPS);  // every warp is done with batch b's slots
+          issue(b + 2);
+        }
+        EPI_STAMP(2);
+        EPI_STAMP(3);
+      } else {
 #pragma unroll 1
         for (int c = c_lo; c < c_end; c += 2) {
           float v[64];
@@ -601,7 +667,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           npend = 0;
         }
       }
-    }, P.sk_first, P.dp_perm);
+    };
+    {
+      SegmentIter it(s, cta, P.num_ctas, dp_lane, P.raster_rows, P.sk_first, P.dp_perm);
+      int64_t u, tile, lb, le, u2 = 0, tile2 = 0, lb2 = 0, le2 = 0;
+      bool have = it.next(s, &u, &tile, &lb, &le);
+      while (have) {
+        const bool more = it.next(s, &u2, &tile2, &lb2, &le2);
+        segment(u, tile, lb, le, !more);
+        u = u2, tile = tile2, lb = lb2, le = le2;
+        have = more;
+      }
+    }
     if (lane == 0) ptx::tma_store_wait_all<0>();
     __syncwarp();
     EPI_STAMP(14);
