@@ -101,10 +101,8 @@ struct Cfg {
   static constexpr int b_off = a_off + STAGES * A_STAGE;
   static constexpr int epi_off = b_off + STAGES * B_STAGE;
   static constexpr int bar_off = epi_off + EPI_BYTES;
-  static constexpr int bar_bytes = (2 * STAGES + 6) * 8 + 16;
-  // Tail fold: the ring's bytes hold 16 KB chunks of peer slabs, two batches.
-  static constexpr int TAIL_SLOT = ROWS * 32 * 4;
-  static constexpr int TAIL_BATCH = epi_off / TAIL_SLOT / 2;
+  static constexpr int bar_bytes = (2 * STAGES + 4) * 8 + 16;
+  static_assert(EPI_WARPS * (EPI_COLS / 32) * EPI_BUF_BYTES <= epi_off, "final-segment C staging fits the ring");
   static constexpr int alloc = bar_off + bar_bytes + 1024;  // + runtime 1 KB alignment
   static_assert(alloc <= 232448, "smem budget");
 };
@@ -183,8 +181,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* empty_bar = full_bar + K::STAGES;
   uint64_t* tfull_bar = empty_bar + K::STAGES;
   uint64_t* tempty_bar = tfull_bar + 2;
-  uint64_t* tail_bar = tempty_bar + 2;
-  uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(tail_bar + 2);
+  uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(tempty_bar + 2);
   int* lane_code_smem = reinterpret_cast<int*>(tmem_base_smem + 1);
 
   const uint32_t warp = threadIdx.x / 32;
@@ -205,7 +202,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&tfull_bar[i], 1);
       ptx::mbar_init(&tempty_bar[i], EPI_WARPS * CG);
-      ptx::mbar_init(&tail_bar[i], 1);
     }
     ptx::fence_barrier_init();
     // Die-aware DP lane (die_lane): keyed by the leader CTA's SM, shared with the peer.
@@ -357,9 +353,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // One 32x32 fp32 box of C (this warp's rows, 32 columns at n0 + 32 * c): stage
     // through a ring of EPI_BUFS swizzled smem boxes (16-B chunk j of row r at
     // j ^ (r % 8)); EPI_BUFS - 1 TMA stores stay in flight while the next is written.
-    auto store_box = [&](const float* v32, int32_t n0, int32_t m0, int c) {
+    // ring = true (the CTA's final segment, ring idle): stage in the smem ring
+    // instead, one 4 KB box per chunk (32 KB per warp), so no store waits for
+    // an earlier one to drain.
+    auto store_box = [&](const float* v32, int32_t n0, int32_t m0, int c, bool ring = false) {
       float* buf = stage_buf + (nstores % EPI_BUFS) * (EPI_BUF_BYTES / 4);
-      if (nstores >= EPI_BUFS) {
+      if (ring) {
+        buf = reinterpret_cast<float*>(smem + (warp - 2) * (EPI_COLS / 32) * EPI_BUF_BYTES +
+                                       (c - c_lo) * EPI_BUF_BYTES);
+      } else if (nstores >= EPI_BUFS) {
         if (lane == 0) ptx::tma_store_wait_read<EPI_BUFS - 1>();
         __syncwarp();
       }
@@ -460,7 +462,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     int64_t pend0 = 0, pend1 = 0;  // this unit's published shared tiles (at most two)
     int npend = 0;
     // final_seg: the CTA's last segment -- its mainloop has drained the smem
-    // ring, which the tail fold below reuses.
+    // ring, which then stages the segment's C boxes (store_box ring mode).
     auto segment = [&](int64_t u, int64_t tile, int64_t lb, int64_t le, bool final_seg) {
       ptx::mbar_wait(&tfull_bar[acc], acc_phase);
       ptx::tc_fence_after();
@@ -480,22 +482,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const bool coop_t = P.coop && (partial || npeer > 0);
       const bool publish = partial || coop_t;
       const int fold_n = coop_t ? 0 : npeer;  // peers this owner folds itself
-      // Tail fold: on the CTA's final segment the owner streams its peers' slabs
-      // into the (now idle) smem ring with bulk copies -- the TMA engine keeps
-      // 96 KB of slab reads in flight instead of the epilogue warps' 32 KB of
-      // register loads -- and the warps fold them from smem (same order).
-      const bool tail = EPI_WARPS == 4 && final_seg && fold_n > 0;
       if (fold_n > 0) {
-        if (tail) {
-          if (leader) {
-            for (int p = 1; p <= fold_n; ++p) wait_flag(P, P.flags + fidx(s.peer(tile, u, p)));
-            ptx::fence_proxy_async_global();  // peers' generic-proxy slab writes -> bulk reads
-          }
-        } else {
-          if (lane == 0)
-            for (int p = 1; p <= fold_n; ++p) wait_flag(P, P.flags + fidx(s.peer(tile, u, p)));
-          __syncwarp();
-        }
+        if (lane == 0)
+          for (int p = 1; p <= fold_n; ++p) wait_flag(P, P.flags + fidx(s.peer(tile, u, p)));
+        __syncwarp();
       }
       if (ev) ev[kEvWaitEnd] = ptx::globaltimer();
       EPI_STAMP(15);
@@ -509,55 +499,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const int c_end = (orphan || m0 + static_cast<int32_t>(q * 32) >= s.m)
                             ? c_lo
                             : imin(c_lo + EPI_COLS / 32, 2 * ceil_div(s.n - n0, 64));
-      if (tail) {
-        // jobs j = (chunk j / fold_n, peer 1 + j % fold_n), chunk-major: each
-        // chunk's peers are folded in ascending id (executor.hpp:165-172).
-        const int nch = m0 >= s.m ? 0 : imin(EPI_COLS / 32, 2 * ceil_div(s.n - n0, 64));
-        const int J = nch * fold_n, NB = (J + K::TAIL_BATCH - 1) / K::TAIL_BATCH;
-        auto issue = [&](int b) {
-          if (!leader || b >= NB) return;
-          const int j0 = b * K::TAIL_BATCH, nj = imin(K::TAIL_BATCH, J - j0);
-          uint64_t* bar = &tail_bar[b & 1];
-          ptx::fence_proxy_async_smem();  // generic reads of the slots precede the refill
-          ptx::mbar_expect_tx(bar, static_cast<uint32_t>(nj * K::TAIL_SLOT));
-          for (int i = 0; i < nj; ++i) {
-            const int j = j0 + i;
-            const float* src = slab(fidx(s.peer(tile, u, 1 + j % fold_n))) + (j / fold_n) * (K::TAIL_SLOT / 4);
-            ptx::bulk_load(smem + ((b & 1) * K::TAIL_BATCH + i) * K::TAIL_SLOT, src, K::TAIL_SLOT, bar);
-          }
-        };
-        issue(0);
-        issue(1);
-        EPI_STAMP(1);
-        float v[32];
-#pragma unroll 1
-        for (int b = 0; b < NB; ++b) {
-          const int j0 = b * K::TAIL_BATCH, nj = imin(K::TAIL_BATCH, J - j0);
-          if (c_end > c_lo) {
-            ptx::mbar_wait(&tail_bar[b & 1], (b >> 1) & 1);
-#pragma unroll 1
-            for (int i = 0; i < nj; ++i) {
-              const int j = j0 + i, ch = j / fold_n, pp = j % fold_n;
-              if (pp == 0) ptx::tmem_ld32(tsrc + ch * 32, v);
-              const float4* sl =
-                  reinterpret_cast<const float4*>(smem + ((b & 1) * K::TAIL_BATCH + i) * K::TAIL_SLOT);
-#pragma unroll
-              for (int jj = 0; jj < 8; ++jj) {
-                const float4 w = sl[jj * ROWS + row];
-                v[4 * jj] += w.x;
-                v[4 * jj + 1] += w.y;
-                v[4 * jj + 2] += w.z;
-                v[4 * jj + 3] += w.w;
-              }
-              if (pp == fold_n - 1) store_box(v, n0, m0, ch);
-            }
-          }
-          ptx::named_bar_sync(1, 32 * EPI_WARPS);  // every warp is done with batch b's slots
-          issue(b + 2);
-        }
-        EPI_STAMP(2);
-        EPI_STAMP(3);
-      } else {
+      {
 #pragma unroll 1
         for (int c = c_lo; c < c_end; c += 2) {
           float v[64];
@@ -596,8 +538,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #endif
             }
             EPI_STAMP(2 + 3 * ((c - c_lo) / 2 % 4));
-            store_box(v, n0, m0, c);
-            store_box(v + 32, n0, m0, c + 1);
+            store_box(v, n0, m0, c, final_seg);
+            store_box(v + 32, n0, m0, c + 1, final_seg);
           }
           EPI_STAMP(3 + 3 * ((c - c_lo) / 2 % 4));
         }

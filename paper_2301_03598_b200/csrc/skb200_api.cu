@@ -104,6 +104,7 @@ DeviceInfo g_dev[64];
 // a launch does not scan the environment ten times.  -1 = unset.
 struct Knobs {
   int die_aware = 0, l2_promo = -1, raster_rows = -1, sk_first = -1, k_align = -1, coop = -1;
+  double coop_min = 8.0;  // mean contributors per shared tile from which the cooperative fixup runs
   int pipeline = 1, pipe_g = -1, pipe_w = -1, pipe_trace = 0;
   bool l2_policy_set = false;
   int l2_policy[4] = {0, 0, 0, 0};
@@ -124,6 +125,7 @@ Knobs read_knobs() {
   k.sk_first = num("SKB200_SK_FIRST", -1);
   k.k_align = num("SKB200_K_ALIGN", -1);
   k.coop = num("SKB200_COOP", -1);
+  if (const char* e = getenv("SKB200_COOP_MIN")) k.coop_min = atof(e);
   k.pipeline = num("SKB200_PIPELINE", 1);
   k.pipe_g = num("SKB200_PIPE_G", -1);
   k.pipe_w = num("SKB200_PIPE_W", -1);
@@ -459,9 +461,9 @@ int kernel_ranks(Kernel k) { return k == Kernel::F16_2SM ? 2 : 1; }
 // Mean number of contributing units over the balanced region's shared tiles
 // (tiles with more than one contributor); 0 when none is shared.
 double mean_contributors(const Schedule& s) {
-  // units of >= ipt/4 iterations give tiles at most ~5 contributors: skip the
+  // units of >= ipt/2 iterations give tiles at most ~3 contributors: skip the
   // scan (it then only runs for schedules with few tiles, g <= p units)
-  if (s.bal.q * 4 >= s.ipt) return 0.0;
+  if (s.bal.q * 2 >= s.ipt) return 0.0;
   int64_t shared = 0, sum = 0;
   for (int64_t t = s.bal.begin / s.ipt; t < s.total_tiles; ++t) {
     int64_t owner, last;
@@ -1016,7 +1018,7 @@ sk_status gemm_impl(const sk_gemm_desc* d, void* ws, size_t ws_bytes, cudaStream
   // publishing and folding after its last segment).
   P.coop = 0;
   if (coop_tiles(kern, s) >= 0 && s.bal.count <= P.num_ctas && !a_ready && !c_done) {
-    P.coop = mean_contributors(s) >= 8.0 ? 1 : 0;
+    P.coop = mean_contributors(s) >= knobs().coop_min ? 1 : 0;
     if (knobs().coop >= 0) P.coop = knobs().coop != 0;
   }
   P.die_aware = 0;
