@@ -102,7 +102,6 @@ struct Cfg {
   static constexpr int epi_off = b_off + STAGES * B_STAGE;
   static constexpr int bar_off = epi_off + EPI_BYTES;
   static constexpr int bar_bytes = (2 * STAGES + 4) * 8 + 16;
-  static_assert(EPI_WARPS * (EPI_COLS / 32) * EPI_BUF_BYTES <= epi_off, "final-segment C staging fits the ring");
   static constexpr int alloc = bar_off + bar_bytes + 1024;  // + runtime 1 KB alignment
   static_assert(alloc <= 232448, "smem budget");
 };
@@ -353,15 +352,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // One 32x32 fp32 box of C (this warp's rows, 32 columns at n0 + 32 * c): stage
     // through a ring of EPI_BUFS swizzled smem boxes (16-B chunk j of row r at
     // j ^ (r % 8)); EPI_BUFS - 1 TMA stores stay in flight while the next is written.
-    // ring = true (the CTA's final segment, ring idle): stage in the smem ring
-    // instead, one 4 KB box per chunk (32 KB per warp), so no store waits for
-    // an earlier one to drain.
-    auto store_box = [&](const float* v32, int32_t n0, int32_t m0, int c, bool ring = false) {
+    auto store_box = [&](const float* v32, int32_t n0, int32_t m0, int c) {
       float* buf = stage_buf + (nstores % EPI_BUFS) * (EPI_BUF_BYTES / 4);
-      if (ring) {
-        buf = reinterpret_cast<float*>(smem + (warp - 2) * (EPI_COLS / 32) * EPI_BUF_BYTES +
-                                       (c - c_lo) * EPI_BUF_BYTES);
-      } else if (nstores >= EPI_BUFS) {
+      if (nstores >= EPI_BUFS) {
         if (lane == 0) ptx::tma_store_wait_read<EPI_BUFS - 1>();
         __syncwarp();
       }
@@ -461,9 +454,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     };
     int64_t pend0 = 0, pend1 = 0;  // this unit's published shared tiles (at most two)
     int npend = 0;
-    // final_seg: the CTA's last segment -- its mainloop has drained the smem
-    // ring, which then stages the segment's C boxes (store_box ring mode).
-    auto segment = [&](int64_t u, int64_t tile, int64_t lb, int64_t le, bool final_seg) {
+    for_each_segment(s, cta, P.num_ctas, dp_lane, P.raster_rows,
+                     [&](int64_t u, int64_t tile, int64_t lb, int64_t le) {
       ptx::mbar_wait(&tfull_bar[acc], acc_phase);
       ptx::tc_fence_after();
       EPI_STAMP(0);
@@ -538,8 +530,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #endif
             }
             EPI_STAMP(2 + 3 * ((c - c_lo) / 2 % 4));
-            store_box(v, n0, m0, c, final_seg);
-            store_box(v + 32, n0, m0, c + 1, final_seg);
+            store_box(v, n0, m0, c);
+            store_box(v + 32, n0, m0, c + 1);
           }
           EPI_STAMP(3 + 3 * ((c - c_lo) / 2 % 4));
         }
@@ -609,18 +601,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           npend = 0;
         }
       }
-    };
-    {
-      SegmentIter it(s, cta, P.num_ctas, dp_lane, P.raster_rows, P.sk_first, P.dp_perm);
-      int64_t u, tile, lb, le, u2 = 0, tile2 = 0, lb2 = 0, le2 = 0;
-      bool have = it.next(s, &u, &tile, &lb, &le);
-      while (have) {
-        const bool more = it.next(s, &u2, &tile2, &lb2, &le2);
-        segment(u, tile, lb, le, !more);
-        u = u2, tile = tile2, lb = lb2, le = le2;
-        have = more;
-      }
-    }
+    }, P.sk_first, P.dp_perm);
     if (lane == 0) ptx::tma_store_wait_all<0>();
     __syncwarp();
     EPI_STAMP(14);
