@@ -72,7 +72,7 @@ constexpr int EPI_WARPS = SKB200_EPI_WARPS;
 // path and cost more than the write-backs they save -- Stream-K picks on the
 // 225 near-regression corpus shapes 1.006x -> 1.024x of DP, 9 -> 0 shapes more
 // than 5 % slower, config 3 1.40 -> 1.42, 8192^3 unchanged
-// (profiles/r02/discard_ab.txt).
+// (profiles/r02/epilogue_ab.txt).
 
 static_assert(EPI_WARPS == 4 || EPI_WARPS == 8, "4 or 8 epilogue warps");
 constexpr int EPI_COLS = BN / (EPI_WARPS / 4);  // accumulator columns per epilogue warp
