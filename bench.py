@@ -55,7 +55,9 @@ def parse(argv=None):
     ap.add_argument("--n", type=int, default=8192)
     ap.add_argument("--k", type=int, default=8192)
     ap.add_argument("--dtype", default="bf16", choices=["bf16", "fp16", "fp64"])
-    ap.add_argument("--variant", default="2sm", choices=["auto", "1sm", "2sm"])
+    ap.add_argument("--variant", default="2smw", choices=["auto", "1sm", "2sm", "2smw"])
+    ap.add_argument("--sweep-variant", default="2sm", choices=["1sm", "2sm", "2smw"],
+                    help="kernel variant of the config-3 / skinny legs (the 256x256 tile by default)")
     ap.add_argument("--tile-group", type=int, default=0,
                     help="sk_gemm_desc.tile_group: 0 = the reference's row-major tile map (default); "
                          "G > 1 / -1 = opt-in grouped layout (experiments)")
@@ -238,6 +240,8 @@ def run_reference_arm(args, rank, world):
         blk, p_dev = (64, 64, 16), 296
     elif args.variant == "2sm":
         blk, p_dev = (256, 256, 64), 74
+    elif args.variant == "2smw":
+        blk, p_dev = (256, 512, 64), 74
     else:
         blk, p_dev = (128, 256, 64), 148
     strategy = STRATS[args.strategy]
@@ -288,7 +292,8 @@ def main():
     ab = {"bf16": sk.DType.BFloat16, "fp16": sk.DType.Float16, "fp64": sk.DType.Float64}[args.dtype]
     tdt = {"bf16": torch.bfloat16, "fp16": torch.float16, "fp64": torch.float64}[args.dtype]
     cdt = torch.float64 if args.dtype == "fp64" else torch.float32
-    variant = {"auto": sk.Variant.Auto, "1sm": sk.Variant.OneSM, "2sm": sk.Variant.TwoSM}[args.variant]
+    variant = {"auto": sk.Variant.Auto, "1sm": sk.Variant.OneSM, "2sm": sk.Variant.TwoSM,
+               "2smw": sk.Variant.TwoSMWide}[args.variant]
     blk = sk.kernel_blocking(ab, variant)
     sms = torch.cuda.get_device_properties(local).multi_processor_count
     strategy = sk.Strategy(STRATS[args.strategy])
@@ -451,15 +456,18 @@ def main():
         from paper_2301_03598_b200 import sweep as sw
 
         shapes, label = (sw.CONFIG4, "config4") if args.dtype == "fp64" else (sw.CONFIG3, "config3")
-        rows = sw.run(shapes, ["data_parallel", "stream_k:auto"], variant, args.dtype)
+        sv = {"1sm": sk.Variant.OneSM, "2sm": sk.Variant.TwoSM,
+              "2smw": sk.Variant.TwoSMWide}[args.sweep_variant] if args.dtype != "fp64" else variant
+        rows = sw.run(shapes, ["data_parallel", "stream_k:auto"], sv, args.dtype)
         summ = sw.summarise(rows)["stream_k:auto"]
         sweep = {"shapes": "%s (%d)" % (label, len(shapes)), "policy": "stream_k:auto (cost model)",
+                 "variant": args.sweep_variant if args.dtype != "fp64" else "dmma",
                  "geomean_sk_vs_dp": summ["geomean_speedup"], "min": summ["min"],
                  "max": summ["max"], "regress_gt_5pct": summ["regress_gt_5pct"]}
         if args.dtype != "fp64":
             # bandwidth-bound skinny shapes (below the ridge): HBM GB/s vs the measured peak
             hbm = load_peaks()[1]
-            srows = sw.run(sw.SKINNY[:2] + sw.SKINNY[4:6], ["data_parallel", "stream_k:auto"], variant,
+            srows = sw.run(sw.SKINNY[:2] + sw.SKINNY[4:6], ["data_parallel", "stream_k:auto"], sv,
                            args.dtype)
             sweep["skinny_hbm"] = [
                 {"shape": [r["m"], r["n"], r["k"]], "strategy": r["strategy"], "g": r["g"],

@@ -75,7 +75,10 @@ typedef enum sk_dtype {
 typedef enum sk_variant {
   SK_VARIANT_AUTO = 0, /* the kernel whose tile equals the blocking; 2-SM by default */
   SK_VARIANT_1SM = 1, /* BF16/FP16: 128x256x64, tcgen05 cta_group::1, persistent grid = #SMs */
-  SK_VARIANT_2SM = 2  /* BF16/FP16: 256x256x64, tcgen05 cta_group::2, persistent grid = #SMs/2 pairs */
+  SK_VARIANT_2SM = 2, /* BF16/FP16: 256x256x64, tcgen05 cta_group::2, persistent grid = #SMs/2 pairs */
+  SK_VARIANT_2SM_WIDE = 3 /* BF16/FP16: 256x512x64, two N=256 cta_group::2 MMAs share each A stage
+                             (48 instead of 64 B of operands per SM per MAC step); one TMEM
+                             accumulator, so the epilogue does not overlap the mainloop */
 } sk_variant;
 
 /* types.hpp:20-27.  alpha/beta carried but ignored (executor.hpp:142,179). */

@@ -213,6 +213,7 @@ class Variant(enum.IntEnum):
     Auto = 0
     OneSM = 1
     TwoSM = 2
+    TwoSMWide = 3  # 256x512x64 (two N=256 MMAs per k step), see skb200.h
 
 
 _STRATEGY_NAMES = {

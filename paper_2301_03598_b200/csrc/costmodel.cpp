@@ -305,7 +305,7 @@ sk_status sk_default_cost_params(sk_dtype ab_type, sk_variant variant, sk_cost_p
   sk_cost_params c{};
   if (ab_type == SK_FLOAT64) {
     c = {0.0, 5.2158, 0.0, 0.71323, 0.95141, 0.62478, 0.3, 0.0};  // costmodel_fp64.json
-  } else if (variant == SK_VARIANT_2SM || variant == SK_VARIANT_AUTO) {
+  } else if (variant == SK_VARIANT_2SM || variant == SK_VARIANT_2SM_WIDE || variant == SK_VARIANT_AUTO) {
     c = {3.9049, 0.9955, 0.4063, 0.3098, 2.3291, 3.3913, 0.2, 0.0, kCoopPeers};
   } else {
     c = {4.2166, 0.24668, 1.8380, 0.42998, 2.6520, 2.8518, 0.2, 0.0, kCoopPeers};  // costmodel_1sm.json

@@ -35,6 +35,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "ptx.cuh"
 #include "schedule.hpp"
 #include "sk_kernel_common.cuh"
@@ -43,7 +45,7 @@ namespace skb200 {
 namespace f16 {
 
 constexpr int ROWS = 128;  // rows per CTA (= TMEM lanes)
-constexpr int BN = 256;    // tile columns (MMA N)
+constexpr int MMA_N = 256; // N of one tcgen05.mma; a tile is BN / MMA_N of them side by side
 constexpr int BK = 64;  // k-depth of one Stream-K iteration (the blocking factor)
 // k-depth of one smem stage: 64 (one iteration) or 32 (half-depth stages: twice
 // as many, released after 2 MMAs instead of 4, A in 64-B swizzle).
@@ -75,18 +77,47 @@ constexpr int EPI_WARPS = SKB200_EPI_WARPS;
 // (profiles/r02/epilogue_ab.txt).
 
 static_assert(EPI_WARPS == 4 || EPI_WARPS == 8, "4 or 8 epilogue warps");
-constexpr int EPI_COLS = BN / (EPI_WARPS / 4);  // accumulator columns per epilogue warp
-constexpr int EPI_BUFS = SKB200_EPI_BUFS;   // 4-KB TMA-store staging boxes per epilogue warp
+// Epilogue variants (A/B knobs): PIPE, the next 64 columns' TMEM load in flight
+// while this step is stored; PAIR, a step's two C boxes under one proxy fence and
+// bulk group; SPLIT_RELEASE (wide tile), hand each accumulator half back as soon
+// as it is read.
+#ifndef SKB200_EPI_PIPE
+#define SKB200_EPI_PIPE 0
+#endif
+#ifndef SKB200_EPI_PAIR
+#define SKB200_EPI_PAIR 0
+#endif
+// LSU_STORE: C leaves through st.global from the staging box instead of TMA stores.
+#ifndef SKB200_LSU_STORE
+#define SKB200_LSU_STORE 0
+#endif
+#ifndef SKB200_SPLIT_RELEASE
+#define SKB200_SPLIT_RELEASE 1
+#endif
+#ifndef SKB200_EPI_BUFS_WIDE
+#define SKB200_EPI_BUFS_WIDE SKB200_EPI_BUFS
+#endif
 constexpr int EPI_BUF_BYTES = 32 * 32 * 4;  // 32 rows x 32 fp32 = 4 KB
-constexpr int EPI_BYTES = EPI_WARPS * EPI_BUFS * EPI_BUF_BYTES;
 constexpr int NUM_THREADS = 64 + 32 * EPI_WARPS;  // 320 (192 with 4 epilogue warps)
-constexpr int TMEM_COLS = 512;                    // 2 x 256-col accumulators
-constexpr int SLAB_ELEMS = ROWS * BN;             // fp32 partial per CTA rank
+constexpr int TMEM_COLS = 512;                    // all of TMEM: 512 fp32 columns x 128 lanes
 constexpr int B_BOX_BYTES = 64 * BKS * 2;         // BKS k-rows x 64 cols
 
-template <int CG>
+// Tile width BN: 256 (one MMA, two TMEM accumulators so a tile's epilogue
+// overlaps the next mainloop) or, 2-SM only, 512 ("wide": two N = 256 MMAs
+// share every A stage, so a CTA loads 48 B of operands per 128x512x64 MAC step
+// instead of 64; one accumulator fills TMEM, so the epilogue no longer overlaps).
+template <int CG, int BN>
 struct Cfg {
+  static_assert(BN == 256 || (BN == 512 && CG == 2), "tile widths: 256, 512 (2-SM)");
+  static constexpr int NMMA = BN / MMA_N;                   // MMAs per 16-deep k step
+  static constexpr int BPM = MMA_N / CG / 64;               // 64-col B boxes per MMA per CTA
+  static constexpr int NACC = TMEM_COLS / BN;               // TMEM accumulators
+  static constexpr int EPI_COLS = BN / (EPI_WARPS / 4);     // accumulator columns per epilogue warp
+  static constexpr int SLAB_ELEMS = ROWS * BN;              // fp32 partial per CTA rank
   static constexpr int B_COLS = BN / CG;                    // B columns held per CTA
+  // 4-KB TMA-store staging boxes per epilogue warp
+  static constexpr int EPI_BUFS = BN == 512 ? SKB200_EPI_BUFS_WIDE : SKB200_EPI_BUFS;
+  static constexpr int EPI_BYTES = EPI_WARPS * EPI_BUFS * EPI_BUF_BYTES;
   static constexpr int A_STAGE = ROWS * BKS * 2;            // 16 KB (BKS = 64)
   static constexpr int B_STAGE = B_COLS * BKS * 2;          // 32 KB (1-SM) / 16 KB (2-SM)
   static constexpr int STAGE = A_STAGE + B_STAGE;
@@ -96,7 +127,11 @@ struct Cfg {
 #ifndef SKB200_STAGES_2SM
 #define SKB200_STAGES_2SM 6
 #endif
-  static constexpr int STAGES = (CG == 1 ? SKB200_STAGES_1SM : SKB200_STAGES_2SM) * SUB;
+#ifndef SKB200_STAGES_WIDE
+#define SKB200_STAGES_WIDE 4
+#endif
+  static constexpr int STAGES =
+      (CG == 1 ? SKB200_STAGES_1SM : (BN == 512 ? SKB200_STAGES_WIDE : SKB200_STAGES_2SM)) * SUB;
   static constexpr int a_off = 0;
   static constexpr int b_off = a_off + STAGES * A_STAGE;
   static constexpr int epi_off = b_off + STAGES * B_STAGE;
@@ -164,12 +199,23 @@ __device__ __forceinline__ void mbar_arrive_remote(uint32_t bar_cluster_addr) {
   } while (0)
 #endif
 
-template <int CG>
+// Column (relative to the tile) of this CTA's B box i: MMA i / BPM, this CTA's
+// 256 / CG columns of it, 64-column box i % BPM.
+template <int CG, int BN>
+__device__ __forceinline__ int32_t b_col_of(int i, uint32_t rank) {
+  using K = Cfg<CG, BN>;
+  return (i / K::BPM) * MMA_N + static_cast<int32_t>(rank) * (MMA_N / CG) + 64 * (i % K::BPM);
+}
+
+template <int CG, int BN>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     sk_gemm_f16(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmC, const KernelParams P) {
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 1000)
-  using K = Cfg<CG>;
+  using K = Cfg<CG, BN>;
+  constexpr int EPI_COLS = K::EPI_COLS;
+  constexpr int SLAB_ELEMS = K::SLAB_ELEMS;
+  constexpr int EPI_BUFS = K::EPI_BUFS;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -189,6 +235,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const uint32_t rank = CG == 2 ? cluster_rank() : 0;
   const bool leader_cta = rank == 0;
   const int64_t cta = CG == 2 ? static_cast<int64_t>(cluster_id_x()) : static_cast<int64_t>(blockIdx.x);
+  auto b_col = [rank](int i) { return b_col_of<CG, BN>(i, rank); };
 
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&tmA);
@@ -242,7 +289,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         int64_t tr, tc;
         s.tile_rc(tile, &tr, &tc);
         const int32_t m0 = static_cast<int32_t>(tr * (ROWS * CG) + rank * ROWS);
-        const int32_t n0 = static_cast<int32_t>(tc * BN + rank * K::B_COLS);
+        const int32_t n0 = static_cast<int32_t>(tc * BN);
         // B panels stream through a data-parallel wave but are revisited at
         // unrelated k offsets by Stream-K units: separate L2 priorities.
         const bool sk_unit = s.strategy == kFixedSplit || s.bal.contains_id(u);
@@ -270,7 +317,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             ptx::tma_load_2d(a_dst, &tmA, &full_bar[stage], k0, m0, pol_a);
 #pragma unroll
             for (int i = 0; i < K::B_COLS / 64; ++i)
-              ptx::tma_load_2d(b_dst + i * B_BOX_BYTES, &tmB, &full_bar[stage], n0 + 64 * i, k0, pol_b);
+              ptx::tma_load_2d(b_dst + i * B_BOX_BYTES, &tmB, &full_bar[stage], n0 + b_col(i), k0, pol_b);
           } else {
             // Both CTAs' bytes land on the leader's full barrier; only the leader arrives.
             if (leader_cta) ptx::mbar_expect_tx(&full_bar[stage], 2 * K::STAGE);
@@ -278,7 +325,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             tma_load_2d_to_leader(a_dst, &tmA, fb, k0, m0, pol_a);
 #pragma unroll
             for (int i = 0; i < K::B_COLS / 64; ++i)
-              tma_load_2d_to_leader(b_dst + i * B_BOX_BYTES, &tmB, fb, n0 + 64 * i, k0, pol_b);
+              tma_load_2d_to_leader(b_dst + i * B_BOX_BYTES, &tmB, fb, n0 + b_col(i), k0, pol_b);
           }
           if (++stage == K::STAGES) {
             stage = 0;
@@ -293,43 +340,89 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // ===================== tcgen05.mma issuer =====================
     if (lane == 0 && leader_cta) {
       uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
+      // One k step (BKS deep) of MMAs j0 .. j1-1 on smem stage `stg`; step index
+      // `si` within the segment (0 = first: overwrite the accumulator).
+      auto issue = [&](uint32_t d_tmem, uint32_t stg, int64_t si, int j0, int j1) {
+        const uint32_t a0 = ptx::smem_u32(sA + stg * K::A_STAGE);
+        const uint32_t b0 = ptx::smem_u32(sB + stg * K::B_STAGE);
+#pragma unroll
+        for (int kk = 0; kk < BKS / UMMA_K; ++kk) {
+          // A: K-major, swizzle = row bytes (128 B at BKS 64, 64 B at 32), +32 B per
+          // 16-element k step; SBO = 8 rows x row bytes.
+          const uint64_t ad = BKS == 64 ? ptx::make_sdesc_sw128(a0 + kk * 32, 16, 1024)
+                                        : ptx::make_sdesc_sw64(a0 + kk * 32, 16, 512);
+          // B: MN-major SW128, +16 k-rows x 128 B per k step; LBO = next 64-col box,
+          // SBO = 8 k-rows x 128 B.  MMA j reads this CTA's boxes j * BPM ..; its
+          // accumulator is TMEM columns j * 256 ..
+#pragma unroll
+          for (int j = 0; j < K::NMMA; ++j) {
+            if (j < j0 || j >= j1) continue;
+            const uint64_t bd =
+                ptx::make_sdesc_sw128(b0 + j * K::BPM * B_BOX_BYTES + kk * 2048, B_BOX_BYTES, 1024);
+            ptx::umma_f16<CG>(d_tmem + j * MMA_N, ad, bd, P.idesc, (si > 0 || kk > 0) ? 1u : 0u);
+          }
+        }
+      };
+      auto release = [&](uint32_t stg) {  // free the smem slot once these MMAs have read it
+        if constexpr (CG == 1) ptx::umma_commit(&empty_bar[stg]);
+        else ptx::umma_commit_mc(&empty_bar[stg], 0x3);
+      };
+      auto advance = [&]() {
+        if (++stage == K::STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      };
       for_each_segment(s, cta, P.num_ctas, dp_lane, P.raster_rows,
                        [&](int64_t u, int64_t tile, int64_t lb, int64_t le) {
-        ptx::mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
-        ptx::tc_fence_after();
-        if (long long* ev = event_slot(P, u, tile)) ev[kEvMacStart] = ptx::globaltimer();
+        const int64_t nsteps = (le - lb) * SUB;
         const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int64_t kb = lb; kb < le; ++kb) {
-          for (int h = 0; h < SUB; ++h) {
+        int64_t si = 0;
+        if constexpr (K::NACC == 1) {
+          // One accumulator (wide tile): the epilogue frees its two 256-column
+          // halves one after the other.  Start the segment on half 0 alone for up
+          // to STAGES steps (the ring holds them), then run those steps' half-1
+          // MMAs once half 1 is drained.  Each half still sees k in order.
+          ptx::mbar_wait(&tempty_bar[0], acc_phase ^ 1);
+          ptx::tc_fence_after();
+          if (long long* ev = event_slot(P, u, tile)) ev[kEvMacStart] = ptx::globaltimer();
+          const int64_t d = nsteps < K::STAGES ? nsteps : K::STAGES;
+          uint32_t st = stage, ph = phase;
+          for (int64_t i = 0; i < d; ++i) {
+            ptx::mbar_wait(&full_bar[st], ph);
+            ptx::tc_fence_after();
+            issue(d_tmem, st, i, 0, 1);
+            if (++st == K::STAGES) {
+              st = 0;
+              ph ^= 1;
+            }
+          }
+          ptx::mbar_wait(&tempty_bar[1], acc_phase ^ 1);
+          ptx::tc_fence_after();
+          for (; si < d; ++si) {
+            issue(d_tmem, stage, si, 1, K::NMMA);
+            release(stage);
+            advance();
+          }
+        } else {
+          ptx::mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+          ptx::tc_fence_after();
+          if (long long* ev = event_slot(P, u, tile)) ev[kEvMacStart] = ptx::globaltimer();
+        }
+        for (; si < nsteps; ++si) {
           ptx::mbar_wait(&full_bar[stage], phase);
           ptx::tc_fence_after();
-          const uint32_t a0 = ptx::smem_u32(sA + stage * K::A_STAGE);
-          const uint32_t b0 = ptx::smem_u32(sB + stage * K::B_STAGE);
-#pragma unroll
-          for (int kk = 0; kk < BKS / UMMA_K; ++kk) {
-            // A: K-major, swizzle = row bytes (128 B at BKS 64, 64 B at 32), +32 B per
-            // 16-element k step; SBO = 8 rows x row bytes.
-            const uint64_t ad = BKS == 64 ? ptx::make_sdesc_sw128(a0 + kk * 32, 16, 1024)
-                                          : ptx::make_sdesc_sw64(a0 + kk * 32, 16, 512);
-            // B: MN-major SW128, +16 k-rows x 128 B per k step; LBO = next 64-col box,
-            // SBO = 8 k-rows x 128 B.
-            const uint64_t bd = ptx::make_sdesc_sw128(b0 + kk * 2048, B_BOX_BYTES, 1024);
-            ptx::umma_f16<CG>(d_tmem, ad, bd, P.idesc, (kb > lb || h > 0 || kk > 0) ? 1u : 0u);
-          }
-          // Free the smem slot(s) once these MMAs have read them.
-          if constexpr (CG == 1) ptx::umma_commit(&empty_bar[stage]);
-          else ptx::umma_commit_mc(&empty_bar[stage], 0x3);
-          if (++stage == K::STAGES) {
-            stage = 0;
-            phase ^= 1;
-          }
-          }
+          issue(d_tmem, stage, si, 0, K::NMMA);
+          release(stage);
+          advance();
         }
         // Accumulator ready for the epilogue warps (of both CTAs for CG = 2).
         if constexpr (CG == 1) ptx::umma_commit(&tfull_bar[acc]);
         else ptx::umma_commit_mc(&tfull_bar[acc], 0x3);
-        acc ^= 1;
-        if (acc == 0) acc_phase ^= 1;
+        if (++acc == K::NACC) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
       }, P.sk_first, P.dp_perm);
     }
     __syncwarp();
@@ -342,6 +435,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     float* partials = static_cast<float*>(P.partials);
     const uint64_t pol_c = ptx::make_policy(P.l2_policy[2]);
     uint32_t acc = 0, acc_phase = 0, nstores = 0;
+    bool pair_pending = false;  // the last bulk group is a store_pair
     // flag / slab index of a (unit, rank): each CTA of a pair runs its own protocol
     auto fidx = [&](int64_t u) { return s.slab_of(u) * CG + rank; };
     const int64_t own_base = s.num_slabs * CG;  // cooperative: owners' published accumulators
@@ -354,7 +448,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // j ^ (r % 8)); EPI_BUFS - 1 TMA stores stay in flight while the next is written.
     auto store_box = [&](const float* v32, int32_t n0, int32_t m0, int c) {
       float* buf = stage_buf + (nstores % EPI_BUFS) * (EPI_BUF_BYTES / 4);
-      if (nstores >= EPI_BUFS) {
+      if (pair_pending) {  // the last group holds every buffer
+        if (lane == 0) ptx::tma_store_wait_read<0>();
+        __syncwarp();
+      } else if (nstores >= EPI_BUFS) {
         if (lane == 0) ptx::tma_store_wait_read<EPI_BUFS - 1>();
         __syncwarp();
       }
@@ -364,13 +461,81 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         *reinterpret_cast<float4*>(buf + lane * 32 + jj * 4) =
             make_float4(v32[4 * j], v32[4 * j + 1], v32[4 * j + 2], v32[4 * j + 3]);
       }
+#if SKB200_LSU_STORE
+      // LSU path: read the box back row-contiguous (8 lanes = one 128-B row
+      // segment) and store it with st.global.v4, 4 rows per instruction; the
+      // buffer is free again right after the read, no bulk group to wait on.
+      __syncwarp();
+      {
+        const int64_t col = static_cast<int64_t>(n0) + c * 32 + (lane & 7) * 4;
+#pragma unroll
+        for (int it = 0; it < 8; ++it) {
+          const int r = it * 4 + static_cast<int>(lane >> 3);
+          const int jj = static_cast<int>(lane & 7) ^ (r & 7);
+          const float4 x = *reinterpret_cast<const float4*>(buf + r * 32 + jj * 4);
+          const int64_t gr = static_cast<int64_t>(m0) + q * 32 + r;
+          if (gr < s.m) {
+            float* dst = P.c_ptr + gr * P.ldc + col;
+            if (col + 4 <= s.n) ptx::st_f4_hint(dst, x, pol_c);
+            else {
+              const float e[4] = {x.x, x.y, x.z, x.w};
+              for (int t = 0; t < 4 && col + t < s.n; ++t) dst[t] = e[t];
+            }
+          }
+        }
+      }
+      __syncwarp();
+#else
       ptx::fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {
+#ifndef SKB200_HACK_NOSTORE  // experiment only (wrong C): epilogue cost without the C stores
         ptx::tma_store_2d_hint(&tmC, buf, n0 + c * 32, m0 + static_cast<int32_t>(q * 32), pol_c);
+#endif
         ptx::tma_store_commit();
       }
       ++nstores;
+#endif
+      pair_pending = false;
+    };
+    // 64 columns of C (chunks c, c + 1) as two boxes under ONE proxy fence and
+    // one bulk group; EPI_BUFS >= 2 holds the pair, the previous group is read first.
+    auto store_pair = [&](const float* v64, int32_t n0, int32_t m0, int c) {
+      if constexpr (EPI_BUFS < 2 || !SKB200_EPI_PAIR) {
+        store_box(v64, n0, m0, c);
+        store_box(v64 + 32, n0, m0, c + 1);
+      } else {
+        const int b0 = static_cast<int>(nstores % EPI_BUFS);
+        if (nstores > 0) {
+          if (lane == 0) ptx::tma_store_wait_read<0>();
+          __syncwarp();
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          float* buf = stage_buf + ((b0 + h) % EPI_BUFS) * (EPI_BUF_BYTES / 4);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int jj = j ^ static_cast<int>(lane & 7);
+            *reinterpret_cast<float4*>(buf + lane * 32 + jj * 4) =
+                make_float4(v64[32 * h + 4 * j], v64[32 * h + 4 * j + 1], v64[32 * h + 4 * j + 2],
+                            v64[32 * h + 4 * j + 3]);
+          }
+        }
+        ptx::fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+#ifndef SKB200_HACK_NOSTORE
+            ptx::tma_store_2d_hint(&tmC, stage_buf + ((b0 + h) % EPI_BUFS) * (EPI_BUF_BYTES / 4),
+                                   n0 + (c + h) * 32, m0 + static_cast<int32_t>(q * 32), pol_c);
+#endif
+          }
+          ptx::tma_store_commit();
+        }
+        nstores += 2;
+        pair_pending = true;
+      }
     };
     // Cooperative fold of one shared tile by contributor u: wait for every
     // contributor's slab, fold the 32-column chunks c = idx, idx + ncon, ...
@@ -491,57 +656,108 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const int c_end = (orphan || m0 + static_cast<int32_t>(q * 32) >= s.m)
                             ? c_lo
                             : imin(c_lo + EPI_COLS / 32, 2 * ceil_div(s.n - n0, 64));
-      {
+      // TMEM hand-back: NACC = 2, the whole accumulator once its last columns are
+      // in registers; NACC = 1 (wide), each 256-column half as soon as this warp
+      // has read its part of it (the MMA warp restarts on half 0 first).
+      auto hand_back = [&](int which) {
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if constexpr (CG == 1) ptx::mbar_arrive(&tempty_bar[which]);
+          else mbar_arrive_remote(mapa(&tempty_bar[which], 0));
+        }
+      };
+      constexpr int H0_END = MMA_N / 32;  // chunks of accumulator half 0
+      bool h0_back = K::NACC == 2;  // NACC = 2: no half to hand back separately
+      auto hand_back_last = [&]() {  // the whole accumulator is in registers
+        if (!h0_back) {
+          hand_back(0);
+          h0_back = true;
+        }
+        hand_back(K::NACC == 1 ? 1 : acc);
+      };
+      constexpr std::true_type kFold{};
+      constexpr std::false_type kNoFold{};
+      auto after_read = [&](int next) {  // chunks [c_lo, next) are in registers
+        if (SKB200_SPLIT_RELEASE && !h0_back && (next >= H0_END || next >= c_end)) {
+          hand_back(0);
+          h0_back = true;
+        }
+      };
+      // One 64-column step on registers r (chunks c, c + 1): publish, or fold the
+      // peers (own accumulator, then peers in ascending id, executor.hpp:165-172)
+      // and store.
+      auto step = [&](uint32_t (&r)[64], int c, auto fold) {
+        float* v = reinterpret_cast<float*>(r);
+        EPI_STAMP(1 + 3 * ((c - c_lo) / 2 % 4));
+        if (!decltype(fold)::value && publish) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            ptx::st_cg_f4(slab_ptr(my_slab, c + j / 8, j % 8, row),
+                          make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
+          EPI_STAMP(2 + 3 * ((c - c_lo) / 2 % 4));
+        } else {
+#pragma unroll 1
+          for (int p = 1; decltype(fold)::value && p <= fold_n; ++p) {
+            float* ps = slab(fidx(s.peer(tile, u, p)));
+            float4 w[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) w[j] = ptx::ld_cg_f4(slab_ptr(ps, c + j / 8, j % 8, row));
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              v[4 * j] += w[j].x;
+              v[4 * j + 1] += w[j].y;
+              v[4 * j + 2] += w[j].z;
+              v[4 * j + 3] += w[j].w;
+            }
+#ifdef SKB200_DISCARD
+            // The slab lines this warp just consumed are dead: drop them from L2
+            // without a DRAM write-back (one lane per 128-B line).
+            __syncwarp();
+            if ((lane & 7) == 0) {
+#pragma unroll
+              for (int j = 0; j < 16; ++j) ptx::discard_l2(slab_ptr(ps, c + j / 8, j % 8, row));
+            }
+#endif
+          }
+          EPI_STAMP(2 + 3 * ((c - c_lo) / 2 % 4));
+          store_pair(v, n0, m0, c);
+        }
+        EPI_STAMP(3 + 3 * ((c - c_lo) / 2 % 4));
+      };
+      // Publish / plain store: software pipeline, the TMEM load of the next 64
+      // columns is in flight while this step's registers are stored.  Owner fold:
+      // one step at a time (its peer loads need the registers).
+      if (fold_n > 0 || !SKB200_EPI_PIPE) {
 #pragma unroll 1
         for (int c = c_lo; c < c_end; c += 2) {
-          float v[64];
-          ptx::tmem_ld64(tsrc + c * 32, v);
-          EPI_STAMP(1 + 3 * ((c - c_lo) / 2 % 4));
-          if (publish) {
-#pragma unroll
-            for (int j = 0; j < 16; ++j)
-              ptx::st_cg_f4(slab_ptr(my_slab, c + j / 8, j % 8, row),
-                            make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
-            EPI_STAMP(2 + 3 * ((c - c_lo) / 2 % 4));
-          } else {
-            // Owner fold, one peer batch per round trip: own accumulator, then
-            // peers in ascending id (executor.hpp:165-172).
-#pragma unroll 1
-            for (int p = 1; p <= fold_n; ++p) {
-              float* ps = slab(fidx(s.peer(tile, u, p)));
-              float4 w[16];
-#pragma unroll
-              for (int j = 0; j < 16; ++j) w[j] = ptx::ld_cg_f4(slab_ptr(ps, c + j / 8, j % 8, row));
-#pragma unroll
-              for (int j = 0; j < 16; ++j) {
-                v[4 * j] += w[j].x;
-                v[4 * j + 1] += w[j].y;
-                v[4 * j + 2] += w[j].z;
-                v[4 * j + 3] += w[j].w;
-              }
-              // The slab lines this warp just consumed are dead: drop them from L2
-              // without a DRAM write-back (one lane per 128-B line).
-              __syncwarp();
-#ifdef SKB200_DISCARD
-              if ((lane & 7) == 0) {
-#pragma unroll
-                for (int j = 0; j < 16; ++j) ptx::discard_l2(slab_ptr(ps, c + j / 8, j % 8, row));
-              }
-#endif
-            }
-            EPI_STAMP(2 + 3 * ((c - c_lo) / 2 % 4));
-            store_box(v, n0, m0, c);
-            store_box(v + 32, n0, m0, c + 1);
-          }
-          EPI_STAMP(3 + 3 * ((c - c_lo) / 2 % 4));
+          uint32_t r[64];
+          ptx::tmem_ld64_issue(tsrc + c * 32, r);
+          ptx::tmem_ld_wait(r);
+          after_read(c + 2);
+          if (c + 2 >= c_end) hand_back_last();
+          if (fold_n > 0) step(r, c, kFold);
+          else step(r, c, kNoFold);
         }
-      }
-      // Accumulator drained: hand the TMEM buffer back to the (leader's) MMA warp.
-      ptx::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        if constexpr (CG == 1) ptx::mbar_arrive(&tempty_bar[acc]);
-        else mbar_arrive_remote(mapa(&tempty_bar[acc], 0));
+        if (c_lo >= c_end) hand_back_last();
+      } else {
+        uint32_t ra[64], rb[64];
+        if (c_lo < c_end) ptx::tmem_ld64_issue(tsrc + c_lo * 32, ra);
+#pragma unroll 1
+        for (int c = c_lo; c < c_end; c += 4) {
+          ptx::tmem_ld_wait(ra);
+          after_read(c + 2);
+          if (c + 2 < c_end) ptx::tmem_ld64_issue(tsrc + (c + 2) * 32, rb);
+          else hand_back_last();
+          step(ra, c, kNoFold);
+          if (c + 2 >= c_end) break;
+          ptx::tmem_ld_wait(rb);
+          after_read(c + 4);
+          if (c + 4 < c_end) ptx::tmem_ld64_issue(tsrc + (c + 4) * 32, ra);
+          else hand_back_last();
+          step(rb, c + 2, kNoFold);
+        }
+        if (c_lo >= c_end) hand_back_last();  // nothing of C in this warp's rows / columns
       }
       if (publish && !orphan) {
         __threadfence();
@@ -554,6 +770,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       EPI_STAMP(13);
       if (!partial) {
         if (P.c_done) {  // this warp's rows of the tile are in HBM: count them for copy-out
+          if (SKB200_LSU_STORE) __threadfence_system();
+          __syncwarp();
           if (lane == 0) {
             ptx::tma_store_wait_all<0>();
             ptx::fence_proxy_async_global();
@@ -585,8 +803,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                       (static_cast<long long>(ptx::smid()) << 16);
         ev[kEvDone] = ptx::globaltimer();
       }
-      acc ^= 1;
-      if (acc == 0) acc_phase ^= 1;
+      if (++acc == K::NACC) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
       // Cooperative: shared tiles are folded once the unit has published all of
       // its segments (at most its first and its last), so no fold ever waits
       // behind this unit's own later mainloop work.
@@ -629,19 +849,19 @@ uint32_t make_idesc_f16(bool bf16, int M, int N) {
          (static_cast<uint32_t>(N >> 3) << 17) | (static_cast<uint32_t>(M >> 4) << 24);
 }
 
-size_t f16_slab_bytes() { return sizeof(float) * f16::SLAB_ELEMS; }
+size_t f16_slab_bytes(int bn) { return sizeof(float) * f16::ROWS * bn; }
 int f16_stage_k() { return f16::BKS; }
 int f16_epilogue_warps() { return f16::EPI_WARPS; }
 
-// Per-device setup of variant CG on the CURRENT device (the caller holds the
+// Per-device setup of kernel (CG, BN) on the CURRENT device (the caller holds the
 // device-state mutex and records that it ran): the dynamic-smem / cluster-size
 // opt-ins, then how many CTAs (1-SM) or CTA pairs (2-SM) can be co-resident --
 // the persistent grid is capped by it (a non-resident unit could be waited on).
-template <int CG>
+template <int CG, int BN>
 static cudaError_t prepare_cg(int sms, int* units) {
-  auto kern = f16::sk_gemm_f16<CG>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       f16::Cfg<CG>::alloc);
+  auto kern = f16::sk_gemm_f16<CG, BN>;
+  using K = f16::Cfg<CG, BN>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, K::alloc);
   if (e != cudaSuccess) return e;
   if (CG == 2) {
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
@@ -649,7 +869,7 @@ static cudaError_t prepare_cg(int sms, int* units) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(static_cast<unsigned>(sms - sms % 2));
     cfg.blockDim = dim3(f16::NUM_THREADS);
-    cfg.dynamicSmemBytes = f16::Cfg<CG>::alloc;
+    cfg.dynamicSmemBytes = K::alloc;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = 2;
@@ -660,23 +880,24 @@ static cudaError_t prepare_cg(int sms, int* units) {
     return cudaOccupancyMaxActiveClusters(units, kern, &cfg);
   }
   int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, f16::NUM_THREADS, f16::Cfg<CG>::alloc);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, f16::NUM_THREADS, K::alloc);
   *units = per_sm * sms;
   return e;
 }
 
-cudaError_t f16_prepare(int cg, int sms, int* units) {
-  return cg == 2 ? prepare_cg<2>(sms, units) : prepare_cg<1>(sms, units);
+cudaError_t f16_prepare(int cg, int bn, int sms, int* units) {
+  if (cg == 1) return prepare_cg<1, 256>(sms, units);
+  return bn == 512 ? prepare_cg<2, 512>(sms, units) : prepare_cg<2, 256>(sms, units);
 }
 
-template <int CG>
+template <int CG, int BN>
 static cudaError_t launch_cg(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
                              const KernelParams& p, int pairs_or_ctas, cudaStream_t stream) {
-  auto kern = f16::sk_gemm_f16<CG>;
+  auto kern = f16::sk_gemm_f16<CG, BN>;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(pairs_or_ctas * CG));
   cfg.blockDim = dim3(f16::NUM_THREADS);
-  cfg.dynamicSmemBytes = f16::Cfg<CG>::alloc;
+  cfg.dynamicSmemBytes = f16::Cfg<CG, BN>::alloc;
   cfg.stream = stream;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -690,9 +911,10 @@ static cudaError_t launch_cg(const CUtensorMap& a, const CUtensorMap& b, const C
   return cudaLaunchKernelEx(&cfg, kern, a, b, c, p);
 }
 
-cudaError_t launch_f16(int cg, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
+cudaError_t launch_f16(int cg, int bn, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
                        const KernelParams& p, int grid, cudaStream_t stream) {
-  return cg == 2 ? launch_cg<2>(a, b, c, p, grid, stream) : launch_cg<1>(a, b, c, p, grid, stream);
+  if (cg == 1) return launch_cg<1, 256>(a, b, c, p, grid, stream);
+  return bn == 512 ? launch_cg<2, 512>(a, b, c, p, grid, stream) : launch_cg<2, 256>(a, b, c, p, grid, stream);
 }
 
 }  // namespace skb200

@@ -92,6 +92,8 @@ struct KernelParams {
   // slabs in the reference's order (owner first, peers ascending), instead of
   // the owner folding every peer slab alone (per-SM bandwidth-bound).
   int32_t coop;
+  float* c_ptr;  // C (fp32, row-major, ldc elements per row) for the LSU epilogue
+  int64_t ldc;
   int32_t die_n[2];
   int16_t die_tab[kMaxSms];
 };

@@ -29,11 +29,11 @@
 namespace skb200 {
 // sk_gemm_f16.cu
 uint32_t make_idesc_f16(bool bf16, int M, int N);
-size_t f16_slab_bytes();
+size_t f16_slab_bytes(int bn);
 int f16_stage_k();
 int f16_epilogue_warps();
-cudaError_t f16_prepare(int cg, int sms, int* units);
-cudaError_t launch_f16(int cg, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
+cudaError_t f16_prepare(int cg, int bn, int sms, int* units);
+cudaError_t launch_f16(int cg, int bn, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
                        const KernelParams& p, int grid, cudaStream_t stream);
 // sk_gemm_f64.cu
 size_t f64_slab_bytes();
@@ -91,7 +91,7 @@ struct DeviceInfo {
   // 1-SM and FP64 kernels, CTA pairs for the 2-SM kernel).  A persistent grid
   // larger than that could leave an owner waiting on a unit whose CTA never
   // becomes resident, so every launch is capped by it.
-  bool f16_ready[3] = {false, false, false};
+  bool f16_ready[3] = {false, false, false};  // per tcgen05 kernel (Kernel enum order)
   int f16_units[3] = {0, 0, 0};
   bool f64_ready = false;
   int f64_per_sm = 0;
@@ -423,7 +423,10 @@ size_t dtype_size(int32_t t) {
 }
 
 // Which kernel serves a descriptor.
-enum class Kernel { F16_1SM, F16_2SM, F64 };
+enum class Kernel { F16_1SM, F16_2SM, F16_2SM_WIDE, F64 };
+bool is_f16(Kernel k) { return k != Kernel::F64; }
+int kernel_cg(Kernel k) { return k == Kernel::F16_1SM ? 1 : 2; }
+int kernel_bn(Kernel k) { return k == Kernel::F16_2SM_WIDE ? 512 : 256; }
 
 sk_status pick_kernel(const sk_gemm_desc* d, Kernel* k) {
   if (d->ab_type == SK_BFLOAT16 || d->ab_type == SK_FLOAT16) {
@@ -432,6 +435,12 @@ sk_status pick_kernel(const sk_gemm_desc* d, Kernel* k) {
         (d->variant == SK_VARIANT_AUTO && d->blocking.blk_m == 128 && d->blocking.blk_n == 256 &&
          d->blocking.blk_k == 64)) {
       *k = Kernel::F16_1SM;
+      return SK_OK;
+    }
+    if (d->variant == SK_VARIANT_2SM_WIDE ||
+        (d->variant == SK_VARIANT_AUTO && d->blocking.blk_m == 256 && d->blocking.blk_n == 512 &&
+         d->blocking.blk_k == 64)) {
+      *k = Kernel::F16_2SM_WIDE;
       return SK_OK;
     }
     if (d->variant == SK_VARIANT_2SM || d->variant == SK_VARIANT_AUTO) {
@@ -451,12 +460,13 @@ sk_status kernel_blocking(Kernel k, sk_blocking* out) {
   switch (k) {
     case Kernel::F16_1SM: *out = {128, 256, 64}; return SK_OK;
     case Kernel::F16_2SM: *out = {256, 256, 64}; return SK_OK;
+    case Kernel::F16_2SM_WIDE: *out = {256, 512, 64}; return SK_OK;
     case Kernel::F64: *out = {64, 64, 16}; return SK_OK;
   }
   return SK_EINVAL;
 }
 
-int kernel_ranks(Kernel k) { return k == Kernel::F16_2SM ? 2 : 1; }
+int kernel_ranks(Kernel k) { return is_f16(k) ? kernel_cg(k) : 1; }
 
 // Mean number of contributing units over the balanced region's shared tiles
 // (tiles with more than one contributor); 0 when none is shared.
@@ -487,8 +497,9 @@ int64_t coop_tiles(Kernel k, const Schedule& s) {
 
 size_t kernel_slab_bytes(Kernel k) {
   switch (k) {
-    case Kernel::F16_1SM: return f16_slab_bytes();
-    case Kernel::F16_2SM: return f16_slab_bytes();
+    case Kernel::F16_1SM:
+    case Kernel::F16_2SM:
+    case Kernel::F16_2SM_WIDE: return f16_slab_bytes(kernel_bn(k));
     case Kernel::F64: return 64 * 64 * sizeof(double);
   }
   return 0;
@@ -885,14 +896,14 @@ sk_status resident_units(int dev, const DeviceInfo& info, Kernel kern, int* out)
     *out = di.f64_per_sm * info.sms;
     return SK_OK;
   }
-  const int cg = kern == Kernel::F16_2SM ? 2 : 1;
-  if (!di.f16_ready[cg]) {
-    cudaError_t e = f16_prepare(cg, info.sms, &di.f16_units[cg]);
+  const int cg = kernel_cg(kern), ki = static_cast<int>(kern);
+  if (!di.f16_ready[ki]) {
+    cudaError_t e = f16_prepare(cg, kernel_bn(kern), info.sms, &di.f16_units[ki]);
     if (e != cudaSuccess) return cuda_fail(e, "sk_gemm_f16 attributes / occupancy");
-    if (di.f16_units[cg] < 1) return fail(SK_ECUDA, "sk_gemm_f16 does not fit on the device");
-    di.f16_ready[cg] = true;
+    if (di.f16_units[ki] < 1) return fail(SK_ECUDA, "sk_gemm_f16 does not fit on the device");
+    di.f16_ready[ki] = true;
   }
-  *out = std::min(di.f16_units[cg], info.sms / cg);
+  *out = std::min(di.f16_units[ki], info.sms / cg);
   return SK_OK;
 }
 
@@ -951,6 +962,8 @@ sk_status gemm_impl(const sk_gemm_desc* d, void* ws, size_t ws_bytes, cudaStream
   P.trace = d->trace;
   P.a_ready = a_ready;
   P.c_done = c_done;
+  P.c_ptr = static_cast<float*>(d->C);
+  P.ldc = d->ldc;
   P.b_ready = pipe ? pipe->b_ready : nullptr;
   P.dp_perm = pipe ? pipe->perm : nullptr;
   P.pipe_g = pipe ? pipe->g : 1;
@@ -1022,12 +1035,12 @@ sk_status gemm_impl(const sk_gemm_desc* d, void* ws, size_t ws_bytes, cudaStream
     if (knobs().coop >= 0) P.coop = knobs().coop != 0;
   }
   P.die_aware = 0;
-  if ((kern == Kernel::F16_1SM || kern == Kernel::F16_2SM) && s.dp_tiles > 0 &&
+  if (is_f16(kern) && s.dp_tiles > 0 &&
       P.num_ctas == info.sms / P.ranks && !a_ready)
     P.die_aware = die_table(dev, strm, P.ranks, &P) ? 1 : 0;
 
-  if (kern == Kernel::F16_1SM || kern == Kernel::F16_2SM) {
-    const int cg = kern == Kernel::F16_2SM ? 2 : 1;
+  if (is_f16(kern)) {
+    const int cg = kernel_cg(kern);
     const CUtensorMapDataType dt = d->ab_type == SK_BFLOAT16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
                                                              : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
     CUtensorMap ta, tb, tc;
@@ -1042,7 +1055,7 @@ sk_status gemm_impl(const sk_gemm_desc* d, void* ws, size_t ws_bytes, cudaStream
                    d->ldc, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B);
     if (st) return st;
     P.idesc = make_idesc_f16(d->ab_type == SK_BFLOAT16, 128 * cg, 256);
-    const cudaError_t e = launch_f16(cg, ta, tb, tc, P, static_cast<int>(P.num_ctas), strm);
+    const cudaError_t e = launch_f16(cg, kernel_bn(kern), ta, tb, tc, P, static_cast<int>(P.num_ctas), strm);
     if (e != cudaSuccess) return cuda_fail(e, cg == 2 ? "sk_gemm_f16<2> launch" : "sk_gemm_f16<1> launch");
     return SK_OK;
   }

@@ -318,7 +318,7 @@ def run(shapes, names, variant, dtype, rank=0, world=1, log_every=0, params=None
     blk = sk.kernel_blocking(ab, variant)
     sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
     # p = co-resident persistent CTAs: pairs for 2-SM, 2 DMMA CTAs per SM for FP64
-    p = 2 * sms if dtype == "fp64" else sms // (2 if variant == sk.Variant.TwoSM else 1)
+    p = 2 * sms if dtype == "fp64" else sms // (1 if variant == sk.Variant.OneSM else 2)
     params = params or sk.default_cost_params(ab, variant)
     ver = Verifier(torch, dtype, force_full=force_full, sample_rows=sample_rows) if verify else None
     rows = []
@@ -341,7 +341,7 @@ def run(shapes, names, variant, dtype, rank=0, world=1, log_every=0, params=None
                          "param": a.param, "tiles_m": a.grid.tiles_m, "tiles_n": a.grid.tiles_n,
                          "g": a.grid_size, "ref": ref_columns(a, p),
                          "variant": "dmma" if dtype == "fp64" else (
-                             "2sm" if variant == sk.Variant.TwoSM else "1sm"),
+                             {sk.Variant.TwoSM: "2sm", sk.Variant.TwoSMWide: "2smw"}.get(variant, "1sm")),
                          "dtype": dtype, "copies": timer.copies, "l2_cold": int(timer.cold),
                          "time_us": t, "tflops": 2.0 * m * n * k / (t * 1e-6) / 1e12,
                          "gbps": algorithmic_bytes(m, n, k, dtype) / (t * 1e-6) / 1e9})
@@ -437,7 +437,7 @@ def main(argv=None):
     ap.add_argument("--lo", type=int, default=128)
     ap.add_argument("--hi", type=int, default=8192)
     ap.add_argument("--seed", type=int, default=0)
-    ap.add_argument("--variant", default="2sm", choices=["1sm", "2sm"])
+    ap.add_argument("--variant", default="2sm", choices=["1sm", "2sm", "2smw"])
     ap.add_argument("--dtype", default="bf16", choices=["bf16", "fp16", "fp64"])
     ap.add_argument("--strategies", default="data_parallel,stream_k,two_tile_sk_dp,dp_one_tile_sk")
     ap.add_argument("--out", default="sweep.csv")
@@ -475,7 +475,7 @@ def main(argv=None):
     else:
         raise SystemExit(f"unknown --shapes {args.shapes}")
     names = args.strategies.split(",")
-    variant = sk.Variant.TwoSM if args.variant == "2sm" else sk.Variant.OneSM
+    variant = {"2sm": sk.Variant.TwoSM, "2smw": sk.Variant.TwoSMWide}.get(args.variant, sk.Variant.OneSM)
     force_full = args.cpu_full == "all" or (args.cpu_full == "auto" and args.shapes != "corpus")
     rows = run(shapes, names, variant, args.dtype, rank, world, args.log_every, seeds=seeds,
                verify=not args.no_verify, force_full=force_full, sample_rows=args.sample_rows)
@@ -498,7 +498,7 @@ def main(argv=None):
                    "world": world, **summarise(allrows)}
         if args.calibrate:
             sms = torch.cuda.get_device_properties(0).multi_processor_count
-            p = 2 * sms if args.dtype == "fp64" else sms // (2 if args.variant == "2sm" else 1)
+            p = 2 * sms if args.dtype == "fp64" else sms // (1 if args.variant == "1sm" else 2)
             params, n = fit_cost_model(allrows, p)
             summary["cost_params"] = params.as_dict()
             summary["calibration_samples"] = n

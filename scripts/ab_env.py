@@ -30,7 +30,7 @@ def main():
     ap.add_argument("--k", type=int, default=8192)
     ap.add_argument("--dtype", default="bf16")
     ap.add_argument("--g", type=int, default=74, help="stream_k grid / hybrid p")
-    ap.add_argument("--variant", default="2sm", choices=["1sm", "2sm"])
+    ap.add_argument("--variant", default="2sm", choices=["1sm", "2sm", "2smw"])
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--rounds", type=int, default=4)
@@ -46,7 +46,7 @@ def main():
     A = (torch.rand(m, pad(k, 8), device="cuda") * 2 - 1).to(tdt)[:, :k]
     B = (torch.rand(k, pad(n, 8), device="cuda") * 2 - 1).to(tdt)[:, :n]
     C = torch.empty(m, pad(n, 4), device="cuda", dtype=torch.float32)[:, :n]
-    V = sk.Variant.TwoSM if args.variant == "2sm" else sk.Variant.OneSM
+    V = {"1sm": sk.Variant.OneSM, "2sm": sk.Variant.TwoSM, "2smw": sk.Variant.TwoSMWide}[args.variant]
     blk = sk.kernel_blocking(ab, V)
     prob = sk.GemmProblem(m, n, k)
     if args.strategy == "data_parallel":

@@ -28,8 +28,8 @@ def main():
     ap.add_argument("--variant", default="2sm")
     ap.add_argument("--g", type=int, default=0)
     args = ap.parse_args()
-    V = sk.Variant.TwoSM if args.variant == "2sm" else sk.Variant.OneSM
-    p = 74 if args.variant == "2sm" else 148
+    V = {"1sm": sk.Variant.OneSM, "2sm": sk.Variant.TwoSM, "2smw": sk.Variant.TwoSMWide}[args.variant]
+    p = 148 if args.variant == "1sm" else 74
     blk = sk.kernel_blocking(sk.DType.BFloat16, V)
     P = sk.GemmProblem(args.m, args.n, args.k)
     a = {"stream_k": lambda: sk.stream_k(P, blk, args.g or p), "data_parallel": lambda: sk.data_parallel(P, blk),

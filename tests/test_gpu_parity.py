@@ -48,11 +48,11 @@ def test_smoke():
     __graft_entry__.smoke()
 
 
-VARIANTS = ["1sm", "2sm"]
+VARIANTS = ["1sm", "2sm", "2smw"]
 
 
 def variant(sk, name):
-    return sk.Variant.OneSM if name == "1sm" else sk.Variant.TwoSM
+    return {"1sm": sk.Variant.OneSM, "2sm": sk.Variant.TwoSM, "2smw": sk.Variant.TwoSMWide}[name]
 
 
 @pytest.mark.parametrize("var", VARIANTS)
@@ -341,12 +341,12 @@ def test_graph_capture(sk, torch_cuda):
     assert torch.equal(C, (A.double() @ B.double()).float())
 
 
-@pytest.mark.parametrize("var", ["1sm", "2sm", "fp64"])
+@pytest.mark.parametrize("var", ["1sm", "2sm", "2smw", "fp64"])
 def test_random_instances_bit_exact(sk, port, var):
     """acceptance.cpp criterion 4 on the device: seeded random problems (dims up to
     700, every decomposition with random knobs) with integer-valued operands are
     bit-exact against the oracle's int64 executor."""
-    rng = np.random.default_rng({"1sm": 11, "2sm": 22, "fp64": 33}[var])
+    rng = np.random.default_rng({"1sm": 11, "2sm": 22, "2smw": 44, "fp64": 33}[var])
     if var == "fp64":
         ab, V, dt = sk.DType.Float64, sk.Variant.Auto, np.float64
     else:
