@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define SKB200_ABI_VERSION 3
+#define SKB200_ABI_VERSION 4
 
 typedef enum sk_status {
   SK_OK = 0,

@@ -85,6 +85,7 @@ def main():
     ap.add_argument("--k", type=int, default=8192)
     ap.add_argument("--variant", default="2smw", choices=list(VARIANTS))
     ap.add_argument("--strategy", default="two_tile_sk_dp")
+    ap.add_argument("--g", type=int, default=0, help="stream_k grid (0 = p)")
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--out", default="")
     args = ap.parse_args()
@@ -97,7 +98,7 @@ def main():
     p = 148 if V == sk.Variant.OneSM else 74
     prob = sk.GemmProblem(m, n, k)
     a = {"data_parallel": lambda: sk.data_parallel(prob, blk),
-         "stream_k": lambda: sk.stream_k(prob, blk, p),
+         "stream_k": lambda: sk.stream_k(prob, blk, args.g or p),
          "stream_k:auto": lambda: sk.auto_stream_k(prob, blk, p),
          "two_tile_sk_dp": lambda: sk.hybrid(prob, blk, p, sk.HybridVariant.TwoTileSkDp),
          "dp_one_tile_sk": lambda: sk.hybrid(prob, blk, p, sk.HybridVariant.DpOneTileSk)}[args.strategy]()

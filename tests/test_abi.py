@@ -51,7 +51,7 @@ def test_sass_is_tcgen05_and_tma(sk):
 
 def test_status_strings_and_version(sk):
     lib = sk.lib()
-    assert lib.sk_abi_version() == 3  # v2: SK_EXPLICIT range tables; v3: tile_group
+    assert lib.sk_abi_version() == 4  # v2: SK_EXPLICIT tables; v3: tile_group; v4: SK_VARIANT_2SM_WIDE
     for code in range(7):
         assert lib.sk_status_string(code)
 
@@ -63,10 +63,28 @@ def test_kernel_blocking_per_precision(sk):
     assert (b.blk_m, b.blk_n, b.blk_k) == (128, 256, 64)
     b = sk.kernel_blocking(sk.DType.Float64)
     assert (b.blk_m, b.blk_n, b.blk_k) == (64, 64, 16)
+    b = sk.kernel_blocking(sk.DType.BFloat16, sk.Variant.TwoSMWide)
+    assert (b.blk_m, b.blk_n, b.blk_k) == (256, 512, 64)
     # AUTO with an explicit 1-SM blocking resolves to the 1-SM kernel
     d = _desc(sk, 512, 512, 512, (128, 256, 64), strategy=0, param=1)
     n = C.c_size_t()
     assert sk.lib().sk_workspace_size(C.byref(d), C.byref(n)) == 0
+
+
+def test_wide_variant_workspace(sk):
+    """SK_VARIANT_2SM_WIDE (256x512x64): AUTO resolves it from the blocking, each
+    Stream-K unit's slab is 2 ranks x 128 x 512 fp32, and a 256x256 blocking
+    under the wide variant is refused (the tile names the kernel)."""
+    lib = sk.lib()
+    n = C.c_size_t()
+    d = _desc(sk, 8192, 8192, 8192, (256, 512, 64), strategy=2, param=74)
+    assert lib.sk_workspace_size(C.byref(d), C.byref(n)) == 0  # AUTO -> wide
+    assert n.value >= 74 * 2 * 128 * 512 * 4
+    d.variant = int(sk.Variant.TwoSMWide)
+    assert lib.sk_workspace_size(C.byref(d), C.byref(n)) == 0
+    d = _desc(sk, 8192, 8192, 8192, (256, 256, 64), strategy=2, param=74)
+    d.variant = int(sk.Variant.TwoSMWide)
+    assert lib.sk_workspace_size(C.byref(d), C.byref(n)) == sk.SK_EUNSUPPORTED
 
 
 def _desc(sk, m, n, k, blk, strategy=2, param=148, ab=3):

@@ -6,8 +6,8 @@
   random_matrix<float>(42), (43) rounded to bf16 feed both sides; >= 256 seeded
   rows of C are checked against the reference's gemm_reference<float>
   (executor.hpp:22-54) under its verify bound 8 eps_f32 k max(|ref|, 1)
-  (executor.hpp:217-239), for DP, stream_k(p) and two_tile_sk_dp(p) on both
-  tcgen05 variants.
+  (executor.hpp:217-239), for DP, stream_k(p), two_tile_sk_dp(p) and the
+  policy on every tcgen05 variant (1-SM, 2-SM, 2-SM wide).
 * The tile -> C map: the device-recorded storer of every block of C is the
   owner (fixup_peers_of front) of tile row * tiles_n + col -- the reference's
   row-major map (executor.hpp:69-70) -- and the pinned (transfer-pipelined)
@@ -86,7 +86,7 @@ def test_float_parity_baseline_sizes(sk, torch_cuda, checker, shape):
     B = sk.random_matrix_device(k, n, 43, sk.DType.Float32, sk.DType.BFloat16)
     Bh = B.float().cpu().numpy()
     want = None
-    for V, p in ((sk.Variant.TwoSM, 74), (sk.Variant.OneSM, 148)):
+    for V, p in ((sk.Variant.TwoSM, 74), (sk.Variant.OneSM, 148), (sk.Variant.TwoSMWide, 74)):
         blk = sk.kernel_blocking(sk.DType.BFloat16, V)
         if want is None:
             want = _rows_reference(checker, A[ridx].float().cpu().numpy(), Bh, blk)
@@ -102,13 +102,13 @@ def test_float_parity_baseline_sizes(sk, torch_cuda, checker, shape):
             assert not bool(torch.isnan(C).any())
 
 
-@pytest.mark.parametrize("var", ["1sm", "2sm"])
+@pytest.mark.parametrize("var", ["1sm", "2sm", "2smw"])
 def test_trace_blocks_follow_row_major_map(sk, torch_cuda, var):
     """Trace section 3: the unit that stored block (r, c) is the owner of tile id
     r * tiles_n + c (executor.hpp:69-70); with the opt-in grouped layout the
     storer follows sk_tile_block instead."""
     torch = torch_cuda
-    V = sk.Variant.OneSM if var == "1sm" else sk.Variant.TwoSM
+    V = {"1sm": sk.Variant.OneSM, "2sm": sk.Variant.TwoSM, "2smw": sk.Variant.TwoSMWide}[var]
     p = 148 if var == "1sm" else 74
     blk = sk.kernel_blocking(sk.DType.BFloat16, V)
     for shape in ((8192, 8192, 1024), (1280, 3840, 512), (2304, 2304, 2048), (1000, 3008, 704)):
