@@ -91,10 +91,6 @@ static_assert(EPI_WARPS == 4 || EPI_WARPS == 8, "4 or 8 epilogue warps");
 #ifndef SKB200_LSU_STORE
 #define SKB200_LSU_STORE 0
 #endif
-// FOLD_PRELOAD: the owner fold requests its first peer's chunk before the TMEM read.
-#ifndef SKB200_FOLD_PRELOAD
-#define SKB200_FOLD_PRELOAD 1
-#endif
 #ifndef SKB200_SPLIT_RELEASE
 #define SKB200_SPLIT_RELEASE 1
 #endif
@@ -691,17 +687,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       // One 64-column step on registers r (chunks c, c + 1): publish, or fold the
       // peers (own accumulator, then peers in ascending id, executor.hpp:165-172)
       // and store.
-      auto step = [&](uint32_t (&r)[64], int c, auto fold, const float4* w1 = nullptr) {
+      auto step = [&](uint32_t (&r)[64], int c, auto fold) {
         float* v = reinterpret_cast<float*>(r);
-        if (w1) {  // peer 1's chunk, loaded before the TMEM read (FOLD_PRELOAD)
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            v[4 * j] += w1[j].x;
-            v[4 * j + 1] += w1[j].y;
-            v[4 * j + 2] += w1[j].z;
-            v[4 * j + 3] += w1[j].w;
-          }
-        }
         EPI_STAMP(1 + 3 * ((c - c_lo) / 2 % 4));
         if (!decltype(fold)::value && publish) {
 #pragma unroll
@@ -711,7 +698,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           EPI_STAMP(2 + 3 * ((c - c_lo) / 2 % 4));
         } else {
 #pragma unroll 1
-          for (int p = w1 ? 2 : 1; decltype(fold)::value && p <= fold_n; ++p) {
+          for (int p = 1; decltype(fold)::value && p <= fold_n; ++p) {
             float* ps = slab(fidx(s.peer(tile, u, p)));
             float4 w[16];
 #pragma unroll
@@ -745,25 +732,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll 1
         for (int c = c_lo; c < c_end; c += 2) {
           uint32_t r[64];
-#if SKB200_FOLD_PRELOAD
-          // Owner fold: the first peer's 64 columns are requested before the TMEM
-          // read, so their L2 latency overlaps it (the add order is unchanged).
-          float4 w1[16];
-          if (fold_n > 0) {
-            float* ps = slab(fidx(s.peer(tile, u, 1)));
-#pragma unroll
-            for (int j = 0; j < 16; ++j) w1[j] = ptx::ld_cg_f4(slab_ptr(ps, c + j / 8, j % 8, row));
-          }
-#endif
           ptx::tmem_ld64_issue(tsrc + c * 32, r);
           ptx::tmem_ld_wait(r);
           after_read(c + 2);
           if (c + 2 >= c_end) hand_back_last();
-#if SKB200_FOLD_PRELOAD
-          if (fold_n > 0) step(r, c, kFold, w1);
-#else
           if (fold_n > 0) step(r, c, kFold);
-#endif
           else step(r, c, kNoFold);
         }
         if (c_lo >= c_end) hand_back_last();
