@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define SKB200_ABI_VERSION 4
+#define SKB200_ABI_VERSION 5
 
 typedef enum sk_status {
   SK_OK = 0,
@@ -199,6 +199,13 @@ typedef struct sk_cost_params {
    * costs like coop_peers + contributors / 8 serial peer folds, not peers - 1
    * (0 = the reference's model: the owner folds every peer). */
   double coop_peers;
+  /* > 0: the kernel's cluster fixup (fixed_split(S), S in {8, 4, 2}, the S
+   * k-chunks of a tile reduced through DSMEM) is a candidate of
+   * sk_select_schedule when every chunk is nonempty, the largest chunk has at
+   * least this many iterations and t * S units are co-resident as clusters of S
+   * on the current device (sk_cluster_capacity); 0 = not a candidate. */
+  double cluster_min_iters;
+  double cluster_kernel; /* the sk_variant those constants describe (1 or 2) */
 } sk_cost_params;
 /* B200-calibrated constants for a kernel family. */
 sk_status sk_default_cost_params(sk_dtype ab_type, sk_variant variant, sk_cost_params* out);
@@ -211,7 +218,9 @@ sk_status sk_select_grid_size(const sk_cost_params* params, const sk_tile_grid_t
 sk_status sk_predict_schedule(const sk_cost_params* params, const sk_tile_grid_t* grid,
                               int32_t strategy, int64_t param, int64_t p, double* out);
 /* The Stream-K policy: argmin over data_parallel, stream_k(1..p) and
- * two_tile_sk_dp(p); data-parallel unless another wins by > margin. */
+ * two_tile_sk_dp(p); data-parallel unless another wins by > margin.  With
+ * cluster_min_iters > 0, fixed_split(S) on the cluster fixup is taken first
+ * when it applies (largest S), measured faster on 95 % of such shapes. */
 sk_status sk_select_schedule(const sk_cost_params* params, const sk_tile_grid_t* grid, int64_t p,
                              int32_t* strategy, int64_t* param);
 /* Non-negative least squares over n >= 6 measured (grid, g, time) samples. */
@@ -259,6 +268,10 @@ sk_status sk_tile_block(const sk_gemm_desc* desc, int64_t tile, int64_t* tile_ro
  * unit a fixup wait points to is resident.  Sets the kernel's per-device
  * attributes on first use. */
 sk_status sk_persistent_capacity(sk_dtype ab_type, sk_variant variant, int32_t device, int32_t* units);
+/* Units (CTAs of the 1-SM kernel, CTA pairs of the 2-SM kernel) co-resident
+ * as clusters of `cluster` units (2, 4 or 8) on `device` (-1 = current): the
+ * capacity of the cluster fixup, fixed_split(S) with t * S <= units. */
+sk_status sk_cluster_capacity(sk_variant variant, int32_t cluster, int32_t device, int32_t* units);
 /* Stream-ordered, asynchronous.  Does not synchronise. */
 sk_status sk_gemm(const sk_gemm_desc* desc, void* workspace, size_t workspace_bytes,
                   void* stream);

@@ -148,6 +148,7 @@ _SIGS = {
                               C.c_void_p, C.c_int64, _P(C.c_int64)]),
     "sk_reload_env": (None, []),
     "sk_persistent_capacity": (C.c_int, [C.c_int, C.c_int, C.c_int32, _P(C.c_int32)]),
+    "sk_cluster_capacity": (C.c_int, [C.c_int, C.c_int32, C.c_int32, _P(C.c_int32)]),
 }
 
 
@@ -466,7 +467,8 @@ class CostParams(C.Structure):
     `margin` = minimum predicted gain before leaving data-parallel."""
     _fields_ = [("e", C.c_double), ("a", C.c_double), ("b", C.c_double), ("c", C.c_double),
                 ("d", C.c_double), ("s", C.c_double), ("margin", C.c_double),
-                ("fit_residual", C.c_double), ("coop_peers", C.c_double)]
+                ("fit_residual", C.c_double), ("coop_peers", C.c_double),
+                ("cluster_min_iters", C.c_double), ("cluster_kernel", C.c_double)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -522,8 +524,12 @@ def auto_stream_k(problem: "GemmProblem", blocking: "BlockingFactors", p: int,
                   params: Optional[CostParams] = None) -> "WorkAssignment":
     """The Stream-K policy (sk_select_schedule): the model's argmin over
     data_parallel, stream_k(g <= p) and two_tile_sk_dp(p), keeping
-    data-parallel unless another schedule is predicted to win by > margin."""
-    params = params or default_cost_params()
+    data-parallel unless another schedule is predicted to win by > margin; on
+    the 1-SM kernel fixed_split(S) with the DSMEM cluster fixup when it applies.
+    Default constants follow the blocking's kernel."""
+    if params is None:
+        v = Variant.OneSM if (blocking.blk_m, blocking.blk_n) == (128, 256) else Variant.TwoSM
+        params = default_cost_params(variant=v)
     grid = tile_grid(problem, blocking)
     s, prm = C.c_int32(), C.c_int64()
     _check(lib().sk_select_schedule(C.byref(params), C.byref(grid._c()), p, C.byref(s),
@@ -565,6 +571,15 @@ def load_matrix(path: str, dtype: DType) -> np.ndarray:
         raise MatrixFileError(lib().sk_io_error().decode())
     _check(st, "load_matrix")
     return out
+
+
+def cluster_capacity(cluster: int, variant: "Variant" = None, device: int = -1) -> int:
+    """Units (1-SM: CTAs, 2-SM: CTA pairs) co-resident as clusters of `cluster`
+    units (2, 4, 8): fixed_split(S) runs the DSMEM cluster fixup when t * S fits."""
+    variant = Variant.TwoSM if variant is None else variant
+    out = C.c_int32()
+    _check(lib().sk_cluster_capacity(int(variant), cluster, device, C.byref(out)), "cluster_capacity")
+    return out.value
 
 
 def persistent_capacity(ab_type: DType = DType.BFloat16, variant: Variant = Variant.TwoSM,

@@ -136,7 +136,7 @@ struct Cfg {
   static constexpr int b_off = a_off + STAGES * A_STAGE;
   static constexpr int epi_off = b_off + STAGES * B_STAGE;
   static constexpr int bar_off = epi_off + EPI_BYTES;
-  static constexpr int bar_bytes = (2 * STAGES + 4) * 8 + 16;
+  static constexpr int bar_bytes = (2 * STAGES + 5) * 8 + 16;
   static constexpr int alloc = bar_off + bar_bytes + 1024;  // + runtime 1 KB alignment
   static_assert(alloc <= 232448, "smem budget");
 };
@@ -150,6 +150,11 @@ __device__ __forceinline__ float4* slab_ptr(float* slab, int c, int j, int row) 
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_nctas() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
   return r;
 }
 __device__ __forceinline__ uint32_t cluster_id_x() {
@@ -226,15 +231,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* empty_bar = full_bar + K::STAGES;
   uint64_t* tfull_bar = empty_bar + K::STAGES;
   uint64_t* tempty_bar = tfull_bar + 2;
-  uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  uint64_t* xfix_bar = tempty_bar + 2;  // cluster fixup: peers' accumulators are in their smem
+  uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(xfix_bar + 1);
   int* lane_code_smem = reinterpret_cast<int*>(tmem_base_smem + 1);
 
   const uint32_t warp = threadIdx.x / 32;
   const uint32_t lane = threadIdx.x % 32;
   const Schedule& s = P.s;
-  const uint32_t rank = CG == 2 ? cluster_rank() : 0;
+  // 2-SM: a CTA pair is cluster ranks (2i, 2i + 1) -- the tcgen05 peer CTAs; a
+  // cluster holds one pair, or S pairs under the cluster fixup.
+  const uint32_t crank = CG == 2 ? cluster_rank() : 0;
+  const uint32_t rank = crank & 1u;        // rank inside the pair
+  const uint32_t pair_base = crank & ~1u;  // cluster rank of the pair's leader
   const bool leader_cta = rank == 0;
-  const int64_t cta = CG == 2 ? static_cast<int64_t>(cluster_id_x()) : static_cast<int64_t>(blockIdx.x);
+  const int64_t cta = CG == 2 ? static_cast<int64_t>(cluster_id_x()) * (cluster_nctas() / 2) + crank / 2
+                              : static_cast<int64_t>(blockIdx.x);
+  const uint16_t pair_mask = static_cast<uint16_t>(0x3u << pair_base);
   auto b_col = [rank](int i) { return b_col_of<CG, BN>(i, rank); };
 
   if (warp == 0 && lane == 0) {
@@ -249,18 +261,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       ptx::mbar_init(&tfull_bar[i], 1);
       ptx::mbar_init(&tempty_bar[i], EPI_WARPS * CG);
     }
+    if (BN == 256 && P.cluster_fix > 1) ptx::mbar_init(xfix_bar, EPI_WARPS * (P.cluster_fix - 1));
     ptx::fence_barrier_init();
     // Die-aware DP lane (die_lane): keyed by the leader CTA's SM, shared with the peer.
     if (P.die_aware && leader_cta) {
       const int code = P.die_tab[ptx::smid()];
       *lane_code_smem = code;
-      if constexpr (CG == 2) st_shared_cluster(mapa(lane_code_smem, 1), code);
+      if constexpr (CG == 2) st_shared_cluster(mapa(lane_code_smem, pair_base + 1), code);
     }
   }
   if (warp == 1) ptx::tmem_alloc<CG>(tmem_base_smem, TMEM_COLS);
   ptx::tc_fence_before();
   __syncthreads();
-  if constexpr (CG == 2) cluster_sync();  // peer barriers initialised before any remote use
+  // peer barriers initialised before any remote use
+  if (CG == 2 || P.cluster_fix > 1) cluster_sync();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_base_smem;
   DpLane dp_lane = default_lane(s, cta, P.num_ctas);
@@ -321,7 +335,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           } else {
             // Both CTAs' bytes land on the leader's full barrier; only the leader arrives.
             if (leader_cta) ptx::mbar_expect_tx(&full_bar[stage], 2 * K::STAGE);
-            const uint32_t fb = mapa(&full_bar[stage], 0);
+            const uint32_t fb = mapa(&full_bar[stage], pair_base);
             tma_load_2d_to_leader(a_dst, &tmA, fb, k0, m0, pol_a);
 #pragma unroll
             for (int i = 0; i < K::B_COLS / 64; ++i)
@@ -365,7 +379,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       };
       auto release = [&](uint32_t stg) {  // free the smem slot once these MMAs have read it
         if constexpr (CG == 1) ptx::umma_commit(&empty_bar[stg]);
-        else ptx::umma_commit_mc(&empty_bar[stg], 0x3);
+        else ptx::umma_commit_mc(&empty_bar[stg], pair_mask);
       };
       auto advance = [&]() {
         if (++stage == K::STAGES) {
@@ -418,7 +432,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         // Accumulator ready for the epilogue warps (of both CTAs for CG = 2).
         if constexpr (CG == 1) ptx::umma_commit(&tfull_bar[acc]);
-        else ptx::umma_commit_mc(&tfull_bar[acc], 0x3);
+        else ptx::umma_commit_mc(&tfull_bar[acc], pair_mask);
         if (++acc == K::NACC) {
           acc = 0;
           acc_phase ^= 1;
@@ -632,6 +646,110 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const int32_t m0 = static_cast<int32_t>(tr * (ROWS * CG) + rank * ROWS);
       const int32_t n0 = static_cast<int32_t>(tc * BN);
       const bool partial = lb != 0;  // not the tile starter (executor.hpp:160)
+      if constexpr (BN == 256) {
+        if (P.cluster_fix > 1) {
+          // Cluster fixup (fixed_split(S), one unit per CTA / CTA pair): the S
+          // units of this cluster are the S k-chunks of this tile, chunk y on
+          // unit slot i = S - 1 - y of the cluster (SegmentIter's descending
+          // ids), so the owner (y = 0) is slot S - 1; slot i is cluster rank
+          // i * CG + (rank in the pair).  1) every CTA parks its 128 accumulator
+          // rows in its own (now idle) operand ring as [64 float4 column
+          // groups][128 rows]; 2) release-arrive on the barrier of every other
+          // slot's CTA holding the same rows; 3) slot i folds column groups
+          // [i * 64/S, (i + 1) * 64/S) of all S accumulators through DSMEM,
+          // owner first, then y = 1, 2, ... (executor.hpp:165-172: the owner
+          // fold's order, so C is bit-identical to it), and TMA-stores them.
+          const int S = P.cluster_fix;
+          const uint32_t cr = cluster_rank();
+          const uint32_t slot = cr / CG, hr = cr % CG;
+          float4* park = reinterpret_cast<float4*>(smem);
+#pragma unroll 1
+          for (int c = 0; c < BN / 32; c += 2) {
+            float v[64];
+            ptx::tmem_ld64(tsrc + c * 32, v);
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              park[(c * 8 + j) * ROWS + row] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          }
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            if constexpr (CG == 1) ptx::mbar_arrive(&tempty_bar[acc]);
+            else mbar_arrive_remote(mapa(&tempty_bar[acc], pair_base));
+            for (int qq = 0; qq < S; ++qq)
+              if (qq != static_cast<int>(slot))
+                ptx::mbar_arrive_cluster(xfix_bar, static_cast<uint32_t>(qq * CG) + hr);
+          }
+          ptx::mbar_wait_cluster(xfix_bar, 0);
+          const int jn = (BN / 4) / S, j0 = static_cast<int>(slot) * jn;
+          const bool rows_in = m0 + static_cast<int32_t>(q * 32) < s.m;
+#pragma unroll 1
+          for (int cb = 0; rows_in && cb < jn / 8; ++cb) {
+            const int jb = j0 + cb * 8;  // first column group of this 32-column chunk
+            if (n0 + jb * 4 >= s.n) break;
+            float4 a[8];
+            // 16 columns of up to 4 contributors in flight per batch, folded in y order
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+#pragma unroll 1
+              for (int y0 = 0; y0 < S; y0 += 4) {
+                float4 w[4][4];
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                  if (y0 + b < S) {
+                    const uint32_t base = mapa(park, static_cast<uint32_t>((S - 1 - (y0 + b)) * CG) + hr);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                      w[b][j] = ptx::ld_dsmem_f4(base + ((jb + 4 * h + j) * ROWS + row) * 16);
+                  }
+                }
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                  if (y0 + b < S) {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                      float4& x = a[4 * h + j];
+                      if (y0 + b == 0) {
+                        x = w[b][j];
+                      } else {
+                        x.x += w[b][j].x; x.y += w[b][j].y; x.z += w[b][j].z; x.w += w[b][j].w;
+                      }
+                    }
+                  }
+                }
+              }
+            }
+            store_box(reinterpret_cast<const float*>(a), n0, m0, jb / 8);
+          }
+          if (leader && rank == 0 && P.trace) {  // ownership / partial counts as the reference's protocol
+            if (partial) {
+              atomicAdd(P.trace + 4 * s.total_tiles + u, 1);
+            } else {
+              const int npeer = s.npeers(tile, u);
+              int* t = P.trace + 4 * tile;
+              t[0] = static_cast<int>(u);
+              t[1] = static_cast<int>(s.peer(tile, u, npeer));
+              t[2] = static_cast<int>(u);
+              t[3] = npeer;
+              P.trace[4 * s.total_tiles + s.grid_size + tr * s.tiles_n + tc] = static_cast<int>(u);
+            }
+          }
+          if (ev) {
+            ev[kEvWaitEnd] = ptx::globaltimer();
+            ev[kEvUnit] = u;
+            ev[kEvTile] = tile;
+            ev[kEvCore] = cta;
+            ev[kEvKind] = (partial ? 1 : 2) | (static_cast<long long>(S - 1) << 8) |
+                          (static_cast<long long>(ptx::smid()) << 16);
+            ev[kEvDone] = ptx::globaltimer();
+          }
+          if (++acc == K::NACC) {
+            acc = 0;
+            acc_phase ^= 1;
+          }
+          return;
+        }
+      }
       const bool orphan = partial && s.orphan(tile);  // explicit table: nobody folds it
       const int npeer = (!partial && (le < s.ipt || s.strategy == kExplicit)) ? s.npeers(tile, u) : 0;
       // Cooperative schedule: the owner of a shared tile publishes its
@@ -664,7 +782,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         __syncwarp();
         if (lane == 0) {
           if constexpr (CG == 1) ptx::mbar_arrive(&tempty_bar[which]);
-          else mbar_arrive_remote(mapa(&tempty_bar[which], 0));
+          else mbar_arrive_remote(mapa(&tempty_bar[which], pair_base));
         }
       };
       constexpr int H0_END = MMA_N / 32;  // chunks of accumulator half 0
@@ -829,7 +947,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   ptx::tc_fence_before();
   __syncthreads();
-  if constexpr (CG == 2) cluster_sync();  // the leader's MMAs touch the peer's smem/TMEM
+  // 2-SM: the leader's MMAs touch the peer's smem/TMEM; cluster fixup: peers read this smem
+  if (CG == 2 || P.cluster_fix > 1) cluster_sync();
   ptx::tc_fence_after();
   if (warp == 1) ptx::tmem_dealloc<CG>(tmem_base, TMEM_COLS);
 #ifndef SKB200_EPI_PROBE
@@ -891,7 +1010,7 @@ cudaError_t f16_prepare(int cg, int bn, int sms, int* units) {
 }
 
 template <int CG, int BN>
-static cudaError_t launch_cg(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
+static cudaError_t launch_cg(int cluster, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
                              const KernelParams& p, int pairs_or_ctas, cudaStream_t stream) {
   auto kern = f16::sk_gemm_f16<CG, BN>;
   cudaLaunchConfig_t cfg{};
@@ -901,7 +1020,7 @@ static cudaError_t launch_cg(const CUtensorMap& a, const CUtensorMap& b, const C
   cfg.stream = stream;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.x = static_cast<unsigned>(cluster);  // CG, or S for the cluster fixup
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -911,10 +1030,41 @@ static cudaError_t launch_cg(const CUtensorMap& a, const CUtensorMap& b, const C
   return cudaLaunchKernelEx(&cfg, kern, a, b, c, p);
 }
 
-cudaError_t launch_f16(int cg, int bn, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
-                       const KernelParams& p, int grid, cudaStream_t stream) {
-  if (cg == 1) return launch_cg<1, 256>(a, b, c, p, grid, stream);
-  return bn == 512 ? launch_cg<2, 512>(a, b, c, p, grid, stream) : launch_cg<2, 256>(a, b, c, p, grid, stream);
+cudaError_t launch_f16(int cg, int bn, int cluster, const CUtensorMap& a, const CUtensorMap& b,
+                       const CUtensorMap& c, const KernelParams& p, int grid, cudaStream_t stream) {
+  if (cg == 1) return launch_cg<1, 256>(cluster, a, b, c, p, grid, stream);
+  return bn == 512 ? launch_cg<2, 512>(cluster, a, b, c, p, grid, stream)
+                   : launch_cg<2, 256>(cluster, a, b, c, p, grid, stream);
+}
+
+// Co-resident clusters of `cluster` CTAs of the 256-wide kernel with CG CTAs per
+// unit (cluster fixup); prepare_cg<CG, 256> has set the smem / cluster opt-ins.
+template <int CG>
+static cudaError_t cluster_capacity_cg(int cluster, int sms, int* clusters) {
+  auto kern = f16::sk_gemm_f16<CG, 256>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       f16::Cfg<CG, 256>::alloc);
+  if (e != cudaSuccess) return e;
+  if (cluster > 8) {
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(sms - sms % cluster));
+  cfg.blockDim = dim3(f16::NUM_THREADS);
+  cfg.dynamicSmemBytes = f16::Cfg<CG, 256>::alloc;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = static_cast<unsigned>(cluster);
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaOccupancyMaxActiveClusters(clusters, kern, &cfg);
+}
+
+cudaError_t f16_cluster_capacity(int cg, int cluster, int sms, int* clusters) {
+  return cg == 2 ? cluster_capacity_cg<2>(cluster, sms, clusters) : cluster_capacity_cg<1>(cluster, sms, clusters);
 }
 
 }  // namespace skb200

@@ -92,6 +92,10 @@ struct KernelParams {
   // slabs in the reference's order (owner first, peers ascending), instead of
   // the owner folding every peer slab alone (per-SM bandwidth-bound).
   int32_t coop;
+  // Cluster fixup (1-SM kernel, fixed_split(s) with s | ipt, one unit per CTA):
+  // the s CTAs of a cluster are the s k-chunks of one tile and reduce through
+  // distributed shared memory instead of global slabs; 0 = off.
+  int32_t cluster_fix;
   float* c_ptr;  // C (fp32, row-major, ldc elements per row) for the LSU epilogue
   int64_t ldc;
   int32_t die_n[2];

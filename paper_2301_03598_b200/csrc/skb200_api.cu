@@ -33,7 +33,8 @@ size_t f16_slab_bytes(int bn);
 int f16_stage_k();
 int f16_epilogue_warps();
 cudaError_t f16_prepare(int cg, int bn, int sms, int* units);
-cudaError_t launch_f16(int cg, int bn, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
+cudaError_t f16_cluster_capacity(int cg, int cluster, int sms, int* clusters);
+cudaError_t launch_f16(int cg, int bn, int cluster, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
                        const KernelParams& p, int grid, cudaStream_t stream);
 // sk_gemm_f64.cu
 size_t f64_slab_bytes();
@@ -93,6 +94,7 @@ struct DeviceInfo {
   // becomes resident, so every launch is capped by it.
   bool f16_ready[3] = {false, false, false};  // per tcgen05 kernel (Kernel enum order)
   int f16_units[3] = {0, 0, 0};
+  int cluster_caps[2][4] = {{-1, -1, -1, -1}, {-1, -1, -1, -1}};  // [cg - 1][S = 2, 4, 8]: clusters
   bool f64_ready = false;
   int f64_per_sm = 0;
 };
@@ -104,6 +106,7 @@ DeviceInfo g_dev[64];
 // a launch does not scan the environment ten times.  -1 = unset.
 struct Knobs {
   int die_aware = 0, l2_promo = -1, raster_rows = -1, sk_first = -1, k_align = -1, coop = -1;
+  int cluster_fix = 1;  // fixed_split on the 1-SM kernel: DSMEM fixup inside a cluster when it fits
   double coop_min = 8.0;  // mean contributors per shared tile from which the cooperative fixup runs
   int pipeline = 1, pipe_g = -1, pipe_w = -1, pipe_trace = 0;
   bool l2_policy_set = false;
@@ -125,6 +128,7 @@ Knobs read_knobs() {
   k.sk_first = num("SKB200_SK_FIRST", -1);
   k.k_align = num("SKB200_K_ALIGN", -1);
   k.coop = num("SKB200_COOP", -1);
+  k.cluster_fix = num("SKB200_CLUSTER_FIX", 1);
   if (const char* e = getenv("SKB200_COOP_MIN")) k.coop_min = atof(e);
   k.pipeline = num("SKB200_PIPELINE", 1);
   k.pipe_g = num("SKB200_PIPE_G", -1);
@@ -907,6 +911,39 @@ sk_status resident_units(int dev, const DeviceInfo& info, Kernel kern, int* out)
   return SK_OK;
 }
 
+// Units (CTAs for 1-SM, CTA pairs for 2-SM) of the 256-wide tcgen05 kernel
+// co-resident as clusters of S units (cluster fixup); 0 if none fit.  Caller
+// holds no lock; resident_units() has set the kernel's attributes.
+int cluster_units(int dev, const DeviceInfo& info, Kernel kern, int S) {
+  const int cg = kernel_cg(kern);
+  const int slot = S == 2 ? 1 : S == 4 ? 2 : 3;
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  DeviceInfo& di = g_dev[dev];
+  int& cap = di.cluster_caps[cg - 1][slot];
+  if (cap < 0) {
+    int c = 0;
+    if (f16_cluster_capacity(cg, S * cg, info.sms, &c) != cudaSuccess) {
+      cudaGetLastError();
+      c = 0;
+    }
+    cap = c;
+  }
+  return cap * S;
+}
+
+// Cluster fixup (256-wide tcgen05 kernels, fixed_split(S)): usable when S is 2,
+// 4 or 8, no k-chunk is empty (every unit of a cluster has a segment: the
+// last chunk [(S-1) ips, ipt) is nonempty) and all t * S units are co-resident
+// as clusters of S units.
+int cluster_fix_for(int dev, const DeviceInfo& info, Kernel kern, const Schedule& s) {
+  if ((kern != Kernel::F16_1SM && kern != Kernel::F16_2SM) || s.strategy != kFixedSplit ||
+      knobs().cluster_fix == 0)
+    return 0;
+  const int64_t S = s.split;
+  if ((S != 2 && S != 4 && S != 8) || (S - 1) * s.ips >= s.ipt) return 0;
+  return s.grid_size <= cluster_units(dev, info, kern, static_cast<int>(S)) ? static_cast<int>(S) : 0;
+}
+
 sk_status gemm_impl(const sk_gemm_desc* d, void* ws, size_t ws_bytes, cudaStream_t strm,
                     const PipeFlags* pipe) {
   const int* a_ready = pipe ? pipe->a_ready : nullptr;
@@ -1034,6 +1071,11 @@ sk_status gemm_impl(const sk_gemm_desc* d, void* ws, size_t ws_bytes, cudaStream
     P.coop = mean_contributors(s) >= knobs().coop_min ? 1 : 0;
     if (knobs().coop >= 0) P.coop = knobs().coop != 0;
   }
+  P.cluster_fix = 0;
+  if (!a_ready && !c_done && !xp) {
+    P.cluster_fix = cluster_fix_for(dev, info, kern, s);
+    if (P.cluster_fix) P.num_ctas = s.grid_size;  // one unit per CTA, clusters of S
+  }
   P.die_aware = 0;
   if (is_f16(kern) && s.dp_tiles > 0 &&
       P.num_ctas == info.sms / P.ranks && !a_ready)
@@ -1055,7 +1097,8 @@ sk_status gemm_impl(const sk_gemm_desc* d, void* ws, size_t ws_bytes, cudaStream
                    d->ldc, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B);
     if (st) return st;
     P.idesc = make_idesc_f16(d->ab_type == SK_BFLOAT16, 128 * cg, 256);
-    const cudaError_t e = launch_f16(cg, kernel_bn(kern), ta, tb, tc, P, static_cast<int>(P.num_ctas), strm);
+    const cudaError_t e = launch_f16(cg, kernel_bn(kern), P.cluster_fix > 1 ? P.cluster_fix * cg : cg, ta, tb, tc, P,
+                                     static_cast<int>(P.num_ctas), strm);
     if (e != cudaSuccess) return cuda_fail(e, cg == 2 ? "sk_gemm_f16<2> launch" : "sk_gemm_f16<1> launch");
     return SK_OK;
   }
@@ -1546,6 +1589,32 @@ extern "C" sk_status sk_execute_ranges(const sk_problem* p, const sk_blocking* b
 }
 
 extern "C" void sk_execute_release(void) { g_exec.release(); }
+
+extern "C" sk_status sk_cluster_capacity(sk_variant variant, int32_t cluster, int32_t device,
+                                         int32_t* units) {
+  if (!units || (cluster != 2 && cluster != 4 && cluster != 8)) return fail(SK_EINVAL, "clusters of 2, 4 or 8 units");
+  if (variant != SK_VARIANT_1SM && variant != SK_VARIANT_2SM)
+    return fail(SK_EUNSUPPORTED, "the cluster fixup runs on the 1-SM and 2-SM 256-wide kernels");
+  *units = 0;
+  int dev = device;
+  if (dev < 0 && cudaGetDevice(&dev) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(SK_ECUDA, "no CUDA device");
+  }
+  DeviceInfo info;
+  sk_status st = device_info(dev, &info);
+  if (st) return st;
+  if (info.cc_major != 10 || info.cc_minor != 0) return fail(SK_EUNSUPPORTED, "sm_100a only");
+  int prev = -1;
+  cudaGetDevice(&prev);
+  if (prev != dev) SK_CUDA(cudaSetDevice(dev));
+  const Kernel kern = variant == SK_VARIANT_1SM ? Kernel::F16_1SM : Kernel::F16_2SM;
+  int resident = 0;
+  st = resident_units(dev, info, kern, &resident);  // kernel attributes first
+  if (!st) *units = cluster_units(dev, info, kern, cluster);
+  if (prev >= 0 && prev != dev) cudaSetDevice(prev);
+  return st;
+}
 
 extern "C" sk_status sk_persistent_capacity(sk_dtype ab_type, sk_variant variant, int32_t device,
                                             int32_t* units) {

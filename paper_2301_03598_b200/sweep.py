@@ -117,6 +117,10 @@ def strategies_for(problem, blk, p, names, params=None):
             out.append(sk.hybrid(problem, blk, p, sk.HybridVariant.DpOneTileSk))
         elif name == "fixed_split":
             out.append(sk.fixed_split(problem, blk, 2))
+        elif name.startswith("fixed_split:"):
+            a = sk.fixed_split(problem, blk, int(name.split(":")[1]))
+            a.label = name
+            out.append(a)
         else:
             raise ValueError(name)
     return out

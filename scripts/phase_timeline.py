@@ -99,6 +99,7 @@ def main():
     prob = sk.GemmProblem(m, n, k)
     a = {"data_parallel": lambda: sk.data_parallel(prob, blk),
          "stream_k": lambda: sk.stream_k(prob, blk, args.g or p),
+         "fixed_split": lambda: sk.fixed_split(prob, blk, args.g or 2),
          "stream_k:auto": lambda: sk.auto_stream_k(prob, blk, p),
          "two_tile_sk_dp": lambda: sk.hybrid(prob, blk, p, sk.HybridVariant.TwoTileSkDp),
          "dp_one_tile_sk": lambda: sk.hybrid(prob, blk, p, sk.HybridVariant.DpOneTileSk)}[args.strategy]()

@@ -51,7 +51,7 @@ def test_sass_is_tcgen05_and_tma(sk):
 
 def test_status_strings_and_version(sk):
     lib = sk.lib()
-    assert lib.sk_abi_version() == 4  # v2: SK_EXPLICIT tables; v3: tile_group; v4: SK_VARIANT_2SM_WIDE
+    assert lib.sk_abi_version() == 5  # v2 SK_EXPLICIT, v3 tile_group, v4 2SM_WIDE, v5 cluster fixup
     for code in range(7):
         assert lib.sk_status_string(code)
 

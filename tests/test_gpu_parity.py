@@ -509,3 +509,48 @@ def test_cooperative_fixup_bit_exact(sk, port, torch_cuda, monkeypatch, shape, g
     sk.reload_env()
     assert np.array_equal(outs["1", "int"], want)
     assert np.array_equal(outs["1", "float"], outs["0", "float"])
+
+
+@pytest.mark.parametrize("var", ["1sm", "2sm"])
+@pytest.mark.parametrize("shape,s", [((128, 8192, 8192), 4), ((128, 8192, 8192), 2), ((129, 264, 1024), 2),
+                                     ((129, 264, 1024), 8), ((256, 512, 4096), 8), ((1000, 1000, 512), 2),
+                                     ((64, 328, 2048), 4), ((300, 1000, 1000), 4)])
+def test_cluster_fixup_fixed_split(sk, port, torch_cuda, monkeypatch, shape, s, var):
+    """fixed_split(s) with no empty k-chunk runs the cluster fixup when t * s
+    units fit as clusters (the s k-chunks of a tile on one cluster, reduced
+    through DSMEM; 1-SM CTAs or 2-SM CTA pairs): integer-valued C bit-exact vs
+    the oracle, float C bit-identical to the global-slab owner fold
+    (SKB200_CLUSTER_FIX=0), and the recorded ownership equal to the
+    reference's fixup_peers_of.  (300 x 1000 x 1000, s = 4: ipt = 16 -> chunks
+    of 4; ragged rows and columns.)"""
+    torch = torch_cuda
+    m, n, k = shape
+    V = variant(sk, var)
+    blk = sk.kernel_blocking(sk.DType.BFloat16, V)
+    a = sk.fixed_split(sk.GemmProblem(m, n, k), blk, s)
+    Ai, Bi = int_operands(port, m, n, k, 91 + k, shift=3 if k > 4096 else 0)
+    want = port.execute("fixed_split", s, Ai, Bi, blk.blk_m, blk.blk_n, blk.blk_k).astype(np.float32)
+    rng = np.random.default_rng(k + s)
+    Af = to_bf16_f32(rng.uniform(-1, 1, (m, k)).astype(np.float32))
+    Bf = to_bf16_f32(rng.uniform(-1, 1, (k, n)).astype(np.float32))
+    owners = [pr[0] for pr in sk.fixup_peers_of(a)]
+    outs = {}
+    for on in ("1", "0"):
+        monkeypatch.setenv("SKB200_CLUSTER_FIX", on)
+        sk.reload_env()
+        gemm = sk.Gemm(a, variant=V, trace=True)
+        for name, (X, Y) in (("int", (Ai, Bi)), ("float", (Af, Bf))):
+            A = torch.from_numpy(X.astype(np.float32)).cuda().to(torch.bfloat16)
+            B = torch.from_numpy(Y.astype(np.float32)).cuda().to(torch.bfloat16)
+            C = torch.full((m, n), float("nan"), device="cuda")
+            for _ in range(2):  # the second launch sees the first one's workspace state
+                gemm.run(A, B, C)
+            gemm.check()
+            outs[on, name] = C.cpu().numpy()
+        storers = gemm.block_storers()
+        assert np.array_equal(storers.reshape(-1), np.array(owners)), on
+    monkeypatch.undo()
+    sk.reload_env()
+    assert np.array_equal(outs["1", "int"], want)
+    assert np.array_equal(outs["0", "int"], want)
+    assert np.array_equal(outs["1", "float"], outs["0", "float"])

@@ -214,3 +214,40 @@ def test_sweep_rows_verified(sk, torch_cuda, which):
         assert all(r["float_check"] == "full" and r["cpu_time_s"] > 0 for r in rows)
     for r in rows:
         assert len(sw.csv_line(r).split(",")) == len(sw.COLUMNS)
+
+
+@pytest.mark.parametrize("var", ["1sm", "2sm"])
+def test_cluster_capacity_and_policy(sk, torch_cuda, checker, var):
+    """The policy takes fixed_split(S) on the DSMEM cluster fixup when t * S
+    units fit as clusters of S and every k-chunk has >= 8 iterations (1-SM
+    CTAs / 2-SM CTA pairs); the wide tile never does.  The result is verified
+    against the reference executor on a row sample."""
+    import oracle
+
+    torch = torch_cuda
+    V = sk.Variant.OneSM if var == "1sm" else sk.Variant.TwoSM
+    p = 148 if var == "1sm" else 74
+    caps = {S: sk.cluster_capacity(S, V) for S in (2, 4, 8)}
+    assert all(0 <= caps[S] <= p and caps[S] % S == 0 for S in caps), caps
+    assert caps[2] > 0
+    blk = sk.kernel_blocking(sk.DType.BFloat16, V)
+    m, n, k = 128, 8192, 8192  # 32 tiles of 128 iterations
+    a = sk.auto_stream_k(sk.GemmProblem(m, n, k), blk, p)
+    t = a.grid.total_tiles
+    want_s = next((S for S in (8, 4, 2) if t * S <= caps[S] and 128 // S >= 8), None)
+    assert want_s is not None
+    assert (a.strategy, a.param) == (sk.Strategy.FixedSplit, want_s)
+    bw = sk.kernel_blocking(sk.DType.BFloat16, sk.Variant.TwoSMWide)
+    aw = sk.auto_stream_k(sk.GemmProblem(m, n, k), bw, 74, sk.default_cost_params(variant=sk.Variant.TwoSMWide))
+    assert aw.strategy != sk.Strategy.FixedSplit
+    A = sk.random_matrix_device(m, k, 42, sk.DType.Float32, sk.DType.BFloat16)
+    B = sk.random_matrix_device(k, n, 43, sk.DType.Float32, sk.DType.BFloat16)
+    C = torch.full((m, n), float("nan"), device="cuda")
+    g = sk.Gemm(a, variant=V)
+    g.run(A, B, C)
+    g.check()
+    rows = np.arange(0, m, 8)
+    want = _rows_reference(checker, A[torch.from_numpy(rows).cuda()].float().cpu().numpy(),
+                           B.float().cpu().numpy(), blk)
+    ok, max_abs, max_rel = oracle.verify(C[torch.from_numpy(rows).cuda()].cpu().numpy(), want, k, EPS32)
+    assert ok, (max_abs, max_rel)
