@@ -470,9 +470,20 @@ def main():
             srows = sw.run(sw.SKINNY[:2] + sw.SKINNY[4:6], ["data_parallel", "stream_k:auto"], sv,
                            args.dtype)
             sweep["skinny_hbm"] = [
-                {"shape": [r["m"], r["n"], r["k"]], "strategy": r["strategy"], "g": r["g"],
+                {"shape": [r["m"], r["n"], r["k"]], "strategy": r["strategy"],
+                 "schedule": r["schedule"], "g": r["g"],
                  "gbps": round(r["gbps"], 1), "frac_of_hbm_peak": round(r["gbps"] / hbm, 3)}
                 for r in srows]
+            if args.sweep_variant != "1sm":
+                # the same shapes on the 1-SM kernel (m <= 128 fills its 128-row tile;
+                # its cluster fixup fits more k-chunks: clusters of up to 8 CTAs)
+                srows = sw.run(sw.SKINNY[:2] + sw.SKINNY[4:6], ["data_parallel", "stream_k:auto"],
+                               sk.Variant.OneSM, args.dtype)
+                sweep["skinny_hbm_1sm"] = [
+                    {"shape": [r["m"], r["n"], r["k"]], "strategy": r["strategy"],
+                     "schedule": r["schedule"], "g": r["g"],
+                     "gbps": round(r["gbps"], 1), "frac_of_hbm_peak": round(r["gbps"] / hbm, 3)}
+                    for r in srows]
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
