@@ -77,19 +77,12 @@ constexpr int EPI_WARPS = SKB200_EPI_WARPS;
 // (profiles/r02/epilogue_ab.txt).
 
 static_assert(EPI_WARPS == 4 || EPI_WARPS == 8, "4 or 8 epilogue warps");
-// Epilogue variants (A/B knobs): PIPE, the next 64 columns' TMEM load in flight
-// while this step is stored; PAIR, a step's two C boxes under one proxy fence and
-// bulk group; SPLIT_RELEASE (wide tile), hand each accumulator half back as soon
-// as it is read.
-#ifndef SKB200_EPI_PIPE
-#define SKB200_EPI_PIPE 0
-#endif
-#ifndef SKB200_EPI_PAIR
-#define SKB200_EPI_PAIR 0
-#endif
-// LSU_STORE: C leaves through st.global from the staging box instead of TMA stores.
-#ifndef SKB200_LSU_STORE
-#define SKB200_LSU_STORE 0
+// SPLIT_RELEASE (wide tile): hand each accumulator half back to the MMA warp as
+// soon as it is read (A/B knob; measured in profiles/r02k/README.txt).
+// CLUSTER_PUSH: the cluster fixup pushes each column slice straight into its
+// folder's smem (remote stores) instead of parking locally and reading remotely.
+#ifndef SKB200_CLUSTER_PUSH
+#define SKB200_CLUSTER_PUSH 1
 #endif
 #ifndef SKB200_SPLIT_RELEASE
 #define SKB200_SPLIT_RELEASE 1
@@ -449,7 +442,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     float* partials = static_cast<float*>(P.partials);
     const uint64_t pol_c = ptx::make_policy(P.l2_policy[2]);
     uint32_t acc = 0, acc_phase = 0, nstores = 0;
-    bool pair_pending = false;  // the last bulk group is a store_pair
     // flag / slab index of a (unit, rank): each CTA of a pair runs its own protocol
     auto fidx = [&](int64_t u) { return s.slab_of(u) * CG + rank; };
     const int64_t own_base = s.num_slabs * CG;  // cooperative: owners' published accumulators
@@ -462,10 +454,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // j ^ (r % 8)); EPI_BUFS - 1 TMA stores stay in flight while the next is written.
     auto store_box = [&](const float* v32, int32_t n0, int32_t m0, int c) {
       float* buf = stage_buf + (nstores % EPI_BUFS) * (EPI_BUF_BYTES / 4);
-      if (pair_pending) {  // the last group holds every buffer
-        if (lane == 0) ptx::tma_store_wait_read<0>();
-        __syncwarp();
-      } else if (nstores >= EPI_BUFS) {
+      if (nstores >= EPI_BUFS) {
         if (lane == 0) ptx::tma_store_wait_read<EPI_BUFS - 1>();
         __syncwarp();
       }
@@ -475,81 +464,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         *reinterpret_cast<float4*>(buf + lane * 32 + jj * 4) =
             make_float4(v32[4 * j], v32[4 * j + 1], v32[4 * j + 2], v32[4 * j + 3]);
       }
-#if SKB200_LSU_STORE
-      // LSU path: read the box back row-contiguous (8 lanes = one 128-B row
-      // segment) and store it with st.global.v4, 4 rows per instruction; the
-      // buffer is free again right after the read, no bulk group to wait on.
-      __syncwarp();
-      {
-        const int64_t col = static_cast<int64_t>(n0) + c * 32 + (lane & 7) * 4;
-#pragma unroll
-        for (int it = 0; it < 8; ++it) {
-          const int r = it * 4 + static_cast<int>(lane >> 3);
-          const int jj = static_cast<int>(lane & 7) ^ (r & 7);
-          const float4 x = *reinterpret_cast<const float4*>(buf + r * 32 + jj * 4);
-          const int64_t gr = static_cast<int64_t>(m0) + q * 32 + r;
-          if (gr < s.m) {
-            float* dst = P.c_ptr + gr * P.ldc + col;
-            if (col + 4 <= s.n) ptx::st_f4_hint(dst, x, pol_c);
-            else {
-              const float e[4] = {x.x, x.y, x.z, x.w};
-              for (int t = 0; t < 4 && col + t < s.n; ++t) dst[t] = e[t];
-            }
-          }
-        }
-      }
-      __syncwarp();
-#else
       ptx::fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {
-#ifndef SKB200_HACK_NOSTORE  // experiment only (wrong C): epilogue cost without the C stores
         ptx::tma_store_2d_hint(&tmC, buf, n0 + c * 32, m0 + static_cast<int32_t>(q * 32), pol_c);
-#endif
         ptx::tma_store_commit();
       }
       ++nstores;
-#endif
-      pair_pending = false;
-    };
-    // 64 columns of C (chunks c, c + 1) as two boxes under ONE proxy fence and
-    // one bulk group; EPI_BUFS >= 2 holds the pair, the previous group is read first.
-    auto store_pair = [&](const float* v64, int32_t n0, int32_t m0, int c) {
-      if constexpr (EPI_BUFS < 2 || !SKB200_EPI_PAIR) {
-        store_box(v64, n0, m0, c);
-        store_box(v64 + 32, n0, m0, c + 1);
-      } else {
-        const int b0 = static_cast<int>(nstores % EPI_BUFS);
-        if (nstores > 0) {
-          if (lane == 0) ptx::tma_store_wait_read<0>();
-          __syncwarp();
-        }
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          float* buf = stage_buf + ((b0 + h) % EPI_BUFS) * (EPI_BUF_BYTES / 4);
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const int jj = j ^ static_cast<int>(lane & 7);
-            *reinterpret_cast<float4*>(buf + lane * 32 + jj * 4) =
-                make_float4(v64[32 * h + 4 * j], v64[32 * h + 4 * j + 1], v64[32 * h + 4 * j + 2],
-                            v64[32 * h + 4 * j + 3]);
-          }
-        }
-        ptx::fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) {
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-#ifndef SKB200_HACK_NOSTORE
-            ptx::tma_store_2d_hint(&tmC, stage_buf + ((b0 + h) % EPI_BUFS) * (EPI_BUF_BYTES / 4),
-                                   n0 + (c + h) * 32, m0 + static_cast<int32_t>(q * 32), pol_c);
-#endif
-          }
-          ptx::tma_store_commit();
-        }
-        nstores += 2;
-        pair_pending = true;
-      }
     };
     // Cooperative fold of one shared tile by contributor u: wait for every
     // contributor's slab, fold the 32-column chunks c = idx, idx + ncon, ...
@@ -663,6 +584,24 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const uint32_t cr = cluster_rank();
           const uint32_t slot = cr / CG, hr = cr % CG;
           float4* park = reinterpret_cast<float4*>(smem);
+          const int jn = (BN / 4) / S, j0 = static_cast<int>(slot) * jn;
+#if SKB200_CLUSTER_PUSH
+          // Push: column group g of this chunk goes straight to slot g / jn's inbox
+          // [S chunks][jn groups][128 rows] (remote stores do not stall), so the
+          // fold below reads only local smem.
+          const int y_me = S - 1 - static_cast<int>(slot);
+#pragma unroll 1
+          for (int c = 0; c < BN / 32; c += 2) {
+            float v[64];
+            ptx::tmem_ld64(tsrc + c * 32, v);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const int g = c * 8 + j, d = g / jn, gl = g - d * jn;
+              ptx::st_dsmem_f4(mapa(park, static_cast<uint32_t>(d * CG) + hr) + ((y_me * jn + gl) * ROWS + row) * 16,
+                               make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
+            }
+          }
+#else
 #pragma unroll 1
           for (int c = 0; c < BN / 32; c += 2) {
             float v[64];
@@ -671,7 +610,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             for (int j = 0; j < 16; ++j)
               park[(c * 8 + j) * ROWS + row] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
           }
+#endif
           ptx::tc_fence_before();
+          ptx::fence_acq_rel_cluster();
           __syncwarp();
           if (lane == 0) {
             if constexpr (CG == 1) ptx::mbar_arrive(&tempty_bar[acc]);
@@ -681,13 +622,27 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 ptx::mbar_arrive_cluster(xfix_bar, static_cast<uint32_t>(qq * CG) + hr);
           }
           ptx::mbar_wait_cluster(xfix_bar, 0);
-          const int jn = (BN / 4) / S, j0 = static_cast<int>(slot) * jn;
+          const long long t_ready = ev ? static_cast<long long>(ptx::globaltimer()) : 0;
           const bool rows_in = m0 + static_cast<int32_t>(q * 32) < s.m;
 #pragma unroll 1
           for (int cb = 0; rows_in && cb < jn / 8; ++cb) {
             const int jb = j0 + cb * 8;  // first column group of this 32-column chunk
             if (n0 + jb * 4 >= s.n) break;
             float4 a[8];
+#if SKB200_CLUSTER_PUSH
+            // local inbox: chunk y's groups [cb * 8, cb * 8 + 8), owner (y = 0) first
+#pragma unroll 1
+            for (int y = 0; y < S; ++y) {
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                const float4 w = park[(y * jn + cb * 8 + j) * ROWS + row];
+                if (y == 0) a[j] = w;
+                else {
+                  a[j].x += w.x; a[j].y += w.y; a[j].z += w.z; a[j].w += w.w;
+                }
+              }
+            }
+#else
             // 16 columns of up to 4 contributors in flight per batch, folded in y order
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
@@ -719,6 +674,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 }
               }
             }
+#endif
             store_box(reinterpret_cast<const float*>(a), n0, m0, jb / 8);
           }
           if (leader && rank == 0 && P.trace) {  // ownership / partial counts as the reference's protocol
@@ -734,8 +690,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               P.trace[4 * s.total_tiles + s.grid_size + tr * s.tiles_n + tc] = static_cast<int>(u);
             }
           }
-          if (ev) {
-            ev[kEvWaitEnd] = ptx::globaltimer();
+          if (ev) {  // MacEnd -> parked, every chunk here (WaitEnd) -> folded, stores issued (Done)
+            ev[kEvWaitEnd] = t_ready;
             ev[kEvUnit] = u;
             ev[kEvTile] = tile;
             ev[kEvCore] = cta;
@@ -839,44 +795,26 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #endif
           }
           EPI_STAMP(2 + 3 * ((c - c_lo) / 2 % 4));
-          store_pair(v, n0, m0, c);
+          store_box(v, n0, m0, c);
+          store_box(v + 32, n0, m0, c + 1);
         }
         EPI_STAMP(3 + 3 * ((c - c_lo) / 2 % 4));
       };
       // Publish / plain store: software pipeline, the TMEM load of the next 64
       // columns is in flight while this step's registers are stored.  Owner fold:
       // one step at a time (its peer loads need the registers).
-      if (fold_n > 0 || !SKB200_EPI_PIPE) {
+      // One 64-column step at a time (a software-pipelined TMEM load measured
+      // slower: profiles/r02k/README.txt).
 #pragma unroll 1
-        for (int c = c_lo; c < c_end; c += 2) {
-          uint32_t r[64];
-          ptx::tmem_ld64_issue(tsrc + c * 32, r);
-          ptx::tmem_ld_wait(r);
-          after_read(c + 2);
-          if (c + 2 >= c_end) hand_back_last();
-          if (fold_n > 0) step(r, c, kFold);
-          else step(r, c, kNoFold);
-        }
-        if (c_lo >= c_end) hand_back_last();
-      } else {
-        uint32_t ra[64], rb[64];
-        if (c_lo < c_end) ptx::tmem_ld64_issue(tsrc + c_lo * 32, ra);
-#pragma unroll 1
-        for (int c = c_lo; c < c_end; c += 4) {
-          ptx::tmem_ld_wait(ra);
-          after_read(c + 2);
-          if (c + 2 < c_end) ptx::tmem_ld64_issue(tsrc + (c + 2) * 32, rb);
-          else hand_back_last();
-          step(ra, c, kNoFold);
-          if (c + 2 >= c_end) break;
-          ptx::tmem_ld_wait(rb);
-          after_read(c + 4);
-          if (c + 4 < c_end) ptx::tmem_ld64_issue(tsrc + (c + 4) * 32, ra);
-          else hand_back_last();
-          step(rb, c + 2, kNoFold);
-        }
-        if (c_lo >= c_end) hand_back_last();  // nothing of C in this warp's rows / columns
+      for (int c = c_lo; c < c_end; c += 2) {
+        uint32_t r[64];
+        ptx::tmem_ld64(tsrc + c * 32, reinterpret_cast<float(&)[64]>(r));
+        after_read(c + 2);
+        if (c + 2 >= c_end) hand_back_last();
+        if (fold_n > 0) step(r, c, kFold);
+        else step(r, c, kNoFold);
       }
+      if (c_lo >= c_end) hand_back_last();  // nothing of C in this warp's rows / columns
       if (publish && !orphan) {
         __threadfence();
         ptx::named_bar_sync(1, 32 * EPI_WARPS);
@@ -888,8 +826,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       EPI_STAMP(13);
       if (!partial) {
         if (P.c_done) {  // this warp's rows of the tile are in HBM: count them for copy-out
-          if (SKB200_LSU_STORE) __threadfence_system();
-          __syncwarp();
           if (lane == 0) {
             ptx::tma_store_wait_all<0>();
             ptx::fence_proxy_async_global();

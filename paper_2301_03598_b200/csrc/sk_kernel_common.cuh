@@ -96,8 +96,6 @@ struct KernelParams {
   // the s CTAs of a cluster are the s k-chunks of one tile and reduce through
   // distributed shared memory instead of global slabs; 0 = off.
   int32_t cluster_fix;
-  float* c_ptr;  // C (fp32, row-major, ldc elements per row) for the LSU epilogue
-  int64_t ldc;
   int32_t die_n[2];
   int16_t die_tab[kMaxSms];
 };

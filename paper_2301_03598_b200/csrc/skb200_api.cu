@@ -999,8 +999,6 @@ sk_status gemm_impl(const sk_gemm_desc* d, void* ws, size_t ws_bytes, cudaStream
   P.trace = d->trace;
   P.a_ready = a_ready;
   P.c_done = c_done;
-  P.c_ptr = static_cast<float*>(d->C);
-  P.ldc = d->ldc;
   P.b_ready = pipe ? pipe->b_ready : nullptr;
   P.dp_perm = pipe ? pipe->perm : nullptr;
   P.pipe_g = pipe ? pipe->g : 1;
