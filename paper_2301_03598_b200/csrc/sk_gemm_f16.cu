@@ -79,11 +79,6 @@ constexpr int EPI_WARPS = SKB200_EPI_WARPS;
 static_assert(EPI_WARPS == 4 || EPI_WARPS == 8, "4 or 8 epilogue warps");
 // SPLIT_RELEASE (wide tile): hand each accumulator half back to the MMA warp as
 // soon as it is read (A/B knob; measured in profiles/r02k/README.txt).
-// CLUSTER_PUSH: the cluster fixup pushes each column slice straight into its
-// folder's smem (remote stores) instead of parking locally and reading remotely.
-#ifndef SKB200_CLUSTER_PUSH
-#define SKB200_CLUSTER_PUSH 1
-#endif
 #ifndef SKB200_SPLIT_RELEASE
 #define SKB200_SPLIT_RELEASE 1
 #endif
@@ -205,7 +200,7 @@ __device__ __forceinline__ int32_t b_col_of(int i, uint32_t rank) {
   return (i / K::BPM) * MMA_N + static_cast<int32_t>(rank) * (MMA_N / CG) + 64 * (i % K::BPM);
 }
 
-template <int CG, int BN>
+template <int CG, int BN, bool CF>  // CF: the cluster-fixup instantiation (fixed_split over DSMEM)
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     sk_gemm_f16(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmC, const KernelParams P) {
@@ -254,7 +249,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       ptx::mbar_init(&tfull_bar[i], 1);
       ptx::mbar_init(&tempty_bar[i], EPI_WARPS * CG);
     }
-    if (BN == 256 && P.cluster_fix > 1) ptx::mbar_init(xfix_bar, EPI_WARPS * (P.cluster_fix - 1));
+    if (CF) ptx::mbar_init(xfix_bar, EPI_WARPS * (P.cluster_fix - 1));
     ptx::fence_barrier_init();
     // Die-aware DP lane (die_lane): keyed by the leader CTA's SM, shared with the peer.
     if (P.die_aware && leader_cta) {
@@ -267,7 +262,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   ptx::tc_fence_before();
   __syncthreads();
   // peer barriers initialised before any remote use
-  if (CG == 2 || P.cluster_fix > 1) cluster_sync();
+  if (CG == 2 || CF) cluster_sync();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_base_smem;
   DpLane dp_lane = default_lane(s, cta, P.num_ctas);
@@ -567,8 +562,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const int32_t m0 = static_cast<int32_t>(tr * (ROWS * CG) + rank * ROWS);
       const int32_t n0 = static_cast<int32_t>(tc * BN);
       const bool partial = lb != 0;  // not the tile starter (executor.hpp:160)
-      if constexpr (BN == 256) {
-        if (P.cluster_fix > 1) {
+      if constexpr (CF) {
+        {
           // Cluster fixup (fixed_split(S), one unit per CTA / CTA pair): the S
           // units of this cluster are the S k-chunks of this tile, chunk y on
           // unit slot i = S - 1 - y of the cluster (SegmentIter's descending
@@ -585,23 +580,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const uint32_t slot = cr / CG, hr = cr % CG;
           float4* park = reinterpret_cast<float4*>(smem);
           const int jn = (BN / 4) / S, j0 = static_cast<int>(slot) * jn;
-#if SKB200_CLUSTER_PUSH
-          // Push: column group g of this chunk goes straight to slot g / jn's inbox
-          // [S chunks][jn groups][128 rows] (remote stores do not stall), so the
-          // fold below reads only local smem.
-          const int y_me = S - 1 - static_cast<int>(slot);
-#pragma unroll 1
-          for (int c = 0; c < BN / 32; c += 2) {
-            float v[64];
-            ptx::tmem_ld64(tsrc + c * 32, v);
-#pragma unroll
-            for (int j = 0; j < 16; ++j) {
-              const int g = c * 8 + j, d = g / jn, gl = g - d * jn;
-              ptx::st_dsmem_f4(mapa(park, static_cast<uint32_t>(d * CG) + hr) + ((y_me * jn + gl) * ROWS + row) * 16,
-                               make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
-            }
-          }
-#else
 #pragma unroll 1
           for (int c = 0; c < BN / 32; c += 2) {
             float v[64];
@@ -610,7 +588,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             for (int j = 0; j < 16; ++j)
               park[(c * 8 + j) * ROWS + row] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
           }
-#endif
           ptx::tc_fence_before();
           ptx::fence_acq_rel_cluster();
           __syncwarp();
@@ -629,20 +606,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const int jb = j0 + cb * 8;  // first column group of this 32-column chunk
             if (n0 + jb * 4 >= s.n) break;
             float4 a[8];
-#if SKB200_CLUSTER_PUSH
-            // local inbox: chunk y's groups [cb * 8, cb * 8 + 8), owner (y = 0) first
-#pragma unroll 1
-            for (int y = 0; y < S; ++y) {
-#pragma unroll
-              for (int j = 0; j < 8; ++j) {
-                const float4 w = park[(y * jn + cb * 8 + j) * ROWS + row];
-                if (y == 0) a[j] = w;
-                else {
-                  a[j].x += w.x; a[j].y += w.y; a[j].z += w.z; a[j].w += w.w;
-                }
-              }
-            }
-#else
             // 16 columns of up to 4 contributors in flight per batch, folded in y order
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
@@ -674,7 +637,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 }
               }
             }
-#endif
             store_box(reinterpret_cast<const float*>(a), n0, m0, jb / 8);
           }
           if (leader && rank == 0 && P.trace) {  // ownership / partial counts as the reference's protocol
@@ -884,7 +846,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   ptx::tc_fence_before();
   __syncthreads();
   // 2-SM: the leader's MMAs touch the peer's smem/TMEM; cluster fixup: peers read this smem
-  if (CG == 2 || P.cluster_fix > 1) cluster_sync();
+  if (CG == 2 || CF) cluster_sync();
   ptx::tc_fence_after();
   if (warp == 1) ptx::tmem_dealloc<CG>(tmem_base, TMEM_COLS);
 #ifndef SKB200_EPI_PROBE
@@ -914,7 +876,7 @@ int f16_epilogue_warps() { return f16::EPI_WARPS; }
 // the persistent grid is capped by it (a non-resident unit could be waited on).
 template <int CG, int BN>
 static cudaError_t prepare_cg(int sms, int* units) {
-  auto kern = f16::sk_gemm_f16<CG, BN>;
+  auto kern = f16::sk_gemm_f16<CG, BN, false>;
   using K = f16::Cfg<CG, BN>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, K::alloc);
   if (e != cudaSuccess) return e;
@@ -945,10 +907,10 @@ cudaError_t f16_prepare(int cg, int bn, int sms, int* units) {
   return bn == 512 ? prepare_cg<2, 512>(sms, units) : prepare_cg<2, 256>(sms, units);
 }
 
-template <int CG, int BN>
+template <int CG, int BN, bool CF>
 static cudaError_t launch_cg(int cluster, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
                              const KernelParams& p, int pairs_or_ctas, cudaStream_t stream) {
-  auto kern = f16::sk_gemm_f16<CG, BN>;
+  auto kern = f16::sk_gemm_f16<CG, BN, CF>;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(pairs_or_ctas * CG));
   cfg.blockDim = dim3(f16::NUM_THREADS);
@@ -968,16 +930,19 @@ static cudaError_t launch_cg(int cluster, const CUtensorMap& a, const CUtensorMa
 
 cudaError_t launch_f16(int cg, int bn, int cluster, const CUtensorMap& a, const CUtensorMap& b,
                        const CUtensorMap& c, const KernelParams& p, int grid, cudaStream_t stream) {
-  if (cg == 1) return launch_cg<1, 256>(cluster, a, b, c, p, grid, stream);
-  return bn == 512 ? launch_cg<2, 512>(cluster, a, b, c, p, grid, stream)
-                   : launch_cg<2, 256>(cluster, a, b, c, p, grid, stream);
+  const bool cf = cluster > cg;  // the cluster fixup: S units per cluster
+  if (cg == 1) return cf ? launch_cg<1, 256, true>(cluster, a, b, c, p, grid, stream)
+                         : launch_cg<1, 256, false>(cluster, a, b, c, p, grid, stream);
+  if (bn == 512) return launch_cg<2, 512, false>(cluster, a, b, c, p, grid, stream);
+  return cf ? launch_cg<2, 256, true>(cluster, a, b, c, p, grid, stream)
+            : launch_cg<2, 256, false>(cluster, a, b, c, p, grid, stream);
 }
 
 // Co-resident clusters of `cluster` CTAs of the 256-wide kernel with CG CTAs per
 // unit (cluster fixup); prepare_cg<CG, 256> has set the smem / cluster opt-ins.
 template <int CG>
 static cudaError_t cluster_capacity_cg(int cluster, int sms, int* clusters) {
-  auto kern = f16::sk_gemm_f16<CG, 256>;
+  auto kern = f16::sk_gemm_f16<CG, 256, true>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        f16::Cfg<CG, 256>::alloc);
   if (e != cudaSuccess) return e;
