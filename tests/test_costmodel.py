@@ -72,9 +72,29 @@ def test_calibrate_recovers_planted(sk):
 def test_auto_stream_k(sk):
     blk = sk.kernel_blocking(sk.DType.BFloat16, sk.Variant.TwoSM)
     p = sk.default_cost_params(sk.DType.BFloat16, sk.Variant.TwoSM)
+    p.cluster_min_iters = 0.0  # the model alone (the cluster rule needs a device)
     # deep-k, few tiles: Stream-K
     a = sk.auto_stream_k(sk.GemmProblem(1024, 1024, 32768), blk, 74, p)
     assert a.strategy == sk.Strategy.StreamK and a.grid_size <= 74
     # small k, many tiles: data-parallel
     a = sk.auto_stream_k(sk.GemmProblem(4096, 4096, 256), blk, 74, p)
     assert a.strategy == sk.Strategy.DataParallel
+
+
+def test_cluster_rule_constants(sk):
+    """The cluster-fixup rule's per-kernel constants: 1-SM chunks >= 8
+    iterations, 2-SM pairs >= 16, off on the wide tile and FP64."""
+    one = sk.default_cost_params(sk.DType.BFloat16, sk.Variant.OneSM)
+    two = sk.default_cost_params(sk.DType.Float16, sk.Variant.TwoSM)
+    wide = sk.default_cost_params(sk.DType.BFloat16, sk.Variant.TwoSMWide)
+    f64 = sk.default_cost_params(sk.DType.Float64, sk.Variant.Auto)
+    assert (one.cluster_min_iters, one.cluster_kernel) == (8.0, 1.0)
+    assert (two.cluster_min_iters, two.cluster_kernel) == (16.0, 2.0)
+    assert wide.cluster_min_iters == 0.0 and f64.cluster_min_iters == 0.0
+    # without a device the rule has no capacity to check and the model decides
+    import torch
+
+    if not torch.cuda.is_available():
+        blk = sk.kernel_blocking(sk.DType.BFloat16, sk.Variant.OneSM)
+        a = sk.auto_stream_k(sk.GemmProblem(128, 8192, 8192), blk, 148)
+        assert a.strategy != sk.Strategy.FixedSplit
