@@ -76,6 +76,13 @@ constexpr int EPI_WARPS = SKB200_EPI_WARPS;
 // than 5 % slower, config 3 1.40 -> 1.42, 8192^3 unchanged
 // (profiles/r02/epilogue_ab.txt).
 
+// Epilogue warps of the wide tile (A/B knob): 8 = two per TMEM lane quarter,
+// interleaved by 64-column steps so both drain half 0 first.  Measured slower
+// than 4 (8192^3 hybrid 1561 vs 1574 TFLOP/s, the inter-tile gap unchanged:
+// profiles/r03b/), so 4.
+#ifndef SKB200_EPI_WARPS_WIDE
+#define SKB200_EPI_WARPS_WIDE 4
+#endif
 static_assert(EPI_WARPS == 4 || EPI_WARPS == 8, "4 or 8 epilogue warps");
 // SPLIT_RELEASE (wide tile): hand each accumulator half back to the MMA warp as
 // soon as it is read (A/B knob; measured in profiles/r02k/README.txt).
@@ -86,7 +93,6 @@ static_assert(EPI_WARPS == 4 || EPI_WARPS == 8, "4 or 8 epilogue warps");
 #define SKB200_EPI_BUFS_WIDE SKB200_EPI_BUFS
 #endif
 constexpr int EPI_BUF_BYTES = 32 * 32 * 4;  // 32 rows x 32 fp32 = 4 KB
-constexpr int NUM_THREADS = 64 + 32 * EPI_WARPS;  // 320 (192 with 4 epilogue warps)
 constexpr int TMEM_COLS = 512;                    // all of TMEM: 512 fp32 columns x 128 lanes
 constexpr int B_BOX_BYTES = 64 * BKS * 2;         // BKS k-rows x 64 cols
 
@@ -100,11 +106,13 @@ struct Cfg {
   static constexpr int NMMA = BN / MMA_N;                   // MMAs per 16-deep k step
   static constexpr int BPM = MMA_N / CG / 64;               // 64-col B boxes per MMA per CTA
   static constexpr int NACC = TMEM_COLS / BN;               // TMEM accumulators
+  static constexpr int EPI_WARPS = BN == 512 ? SKB200_EPI_WARPS_WIDE : SKB200_EPI_WARPS;
+  static constexpr int NUM_THREADS = 64 + 32 * EPI_WARPS;   // 192 (4 epilogue warps) or 320
   static constexpr int EPI_COLS = BN / (EPI_WARPS / 4);     // accumulator columns per epilogue warp
   static constexpr int SLAB_ELEMS = ROWS * BN;              // fp32 partial per CTA rank
   static constexpr int B_COLS = BN / CG;                    // B columns held per CTA
   // 4-KB TMA-store staging boxes per epilogue warp
-  static constexpr int EPI_BUFS = BN == 512 ? SKB200_EPI_BUFS_WIDE : SKB200_EPI_BUFS;
+  static constexpr int EPI_BUFS = EPI_WARPS == 8 ? 1 : (BN == 512 ? SKB200_EPI_BUFS_WIDE : SKB200_EPI_BUFS);
   static constexpr int EPI_BYTES = EPI_WARPS * EPI_BUFS * EPI_BUF_BYTES;
   static constexpr int A_STAGE = ROWS * BKS * 2;            // 16 KB (BKS = 64)
   static constexpr int B_STAGE = B_COLS * BKS * 2;          // 32 KB (1-SM) / 16 KB (2-SM)
@@ -201,12 +209,13 @@ __device__ __forceinline__ int32_t b_col_of(int i, uint32_t rank) {
 }
 
 template <int CG, int BN, bool CF>  // CF: the cluster-fixup instantiation (fixed_split over DSMEM)
-__global__ void __launch_bounds__(NUM_THREADS, 1)
+__global__ void __launch_bounds__(Cfg<CG, BN>::NUM_THREADS, 1)
     sk_gemm_f16(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmC, const KernelParams P) {
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 1000)
   using K = Cfg<CG, BN>;
   constexpr int EPI_COLS = K::EPI_COLS;
+  constexpr int EPI_WARPS = K::EPI_WARPS;
   constexpr int SLAB_ELEMS = K::SLAB_ELEMS;
   constexpr int EPI_BUFS = K::EPI_BUFS;
   extern __shared__ uint8_t smem_raw[];
@@ -443,7 +452,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int64_t done_base = 2 * s.num_slabs * CG;
     const int64_t bal_tile0 = s.bal.begin / s.ipt;
     auto slab = [&](int64_t idx) { return partials + idx * static_cast<int64_t>(SLAB_ELEMS); };
-    const int c_lo = static_cast<int>((warp - 2) / 4) * (EPI_COLS / 32);
+    // epilogue warp group (two groups share each TMEM lane quarter with 8 warps)
+    const int grp = static_cast<int>((warp - 2) / 4);
+    constexpr int NG = EPI_WARPS / 4;
+    const int c_lo = grp * (EPI_COLS / 32);  // cooperative fold: this group's contiguous columns
     // One 32x32 fp32 box of C (this warp's rows, 32 columns at n0 + 32 * c): stage
     // through a ring of EPI_BUFS swizzled smem boxes (16-B chunk j of row r at
     // j ^ (r % 8)); EPI_BUFS - 1 TMA stores stay in flight while the next is written.
@@ -689,9 +701,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       // Only chunks that hold part of C: this warp's 32 rows and the 64-column
       // steps left of n (ragged edges, skinny m or n); every contributor of the
       // tile skips the same (rows, chunk) pairs, so publish and fold stay matched.
+      // 64-column steps c = 2 grp, 2 grp + 2 NG, ... below c_end (32-column chunks).
       const int c_end = (orphan || m0 + static_cast<int32_t>(q * 32) >= s.m)
-                            ? c_lo
-                            : imin(c_lo + EPI_COLS / 32, 2 * ceil_div(s.n - n0, 64));
+                            ? 0
+                            : imin(BN / 32, 2 * ceil_div(s.n - n0, 64));
+      const int c_first = 2 * grp;
       // TMEM hand-back: NACC = 2, the whole accumulator once its last columns are
       // in registers; NACC = 1 (wide), each 256-column half as soon as this warp
       // has read its part of it (the MMA warp restarts on half 0 first).
@@ -714,7 +728,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       };
       constexpr std::true_type kFold{};
       constexpr std::false_type kNoFold{};
-      auto after_read = [&](int next) {  // chunks [c_lo, next) are in registers
+      auto after_read = [&](int next) {  // this warp's chunks below `next` are in registers
         if (SKB200_SPLIT_RELEASE && !h0_back && (next >= H0_END || next >= c_end)) {
           hand_back(0);
           h0_back = true;
@@ -725,13 +739,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       // and store.
       auto step = [&](uint32_t (&r)[64], int c, auto fold) {
         float* v = reinterpret_cast<float*>(r);
-        EPI_STAMP(1 + 3 * ((c - c_lo) / 2 % 4));
+        EPI_STAMP(1 + 3 * (c / 2 % 4));
         if (!decltype(fold)::value && publish) {
 #pragma unroll
           for (int j = 0; j < 16; ++j)
             ptx::st_cg_f4(slab_ptr(my_slab, c + j / 8, j % 8, row),
                           make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
-          EPI_STAMP(2 + 3 * ((c - c_lo) / 2 % 4));
+          EPI_STAMP(2 + 3 * (c / 2 % 4));
         } else {
 #pragma unroll 1
           for (int p = 1; decltype(fold)::value && p <= fold_n; ++p) {
@@ -756,11 +770,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
 #endif
           }
-          EPI_STAMP(2 + 3 * ((c - c_lo) / 2 % 4));
+          EPI_STAMP(2 + 3 * (c / 2 % 4));
           store_box(v, n0, m0, c);
           store_box(v + 32, n0, m0, c + 1);
         }
-        EPI_STAMP(3 + 3 * ((c - c_lo) / 2 % 4));
+        EPI_STAMP(3 + 3 * (c / 2 % 4));
       };
       // Publish / plain store: software pipeline, the TMEM load of the next 64
       // columns is in flight while this step's registers are stored.  Owner fold:
@@ -768,15 +782,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       // One 64-column step at a time (a software-pipelined TMEM load measured
       // slower: profiles/r02k/README.txt).
 #pragma unroll 1
-      for (int c = c_lo; c < c_end; c += 2) {
+      for (int c = c_first; c < c_end; c += 2 * NG) {
         uint32_t r[64];
         ptx::tmem_ld64(tsrc + c * 32, reinterpret_cast<float(&)[64]>(r));
-        after_read(c + 2);
-        if (c + 2 >= c_end) hand_back_last();
+        after_read(c + 2 * NG);
+        if (c + 2 * NG >= c_end) hand_back_last();
         if (fold_n > 0) step(r, c, kFold);
         else step(r, c, kNoFold);
       }
-      if (c_lo >= c_end) hand_back_last();  // nothing of C in this warp's rows / columns
+      if (c_first >= c_end) hand_back_last();  // nothing of C in this warp's rows / columns
       if (publish && !orphan) {
         __threadfence();
         ptx::named_bar_sync(1, 32 * EPI_WARPS);
@@ -868,7 +882,9 @@ uint32_t make_idesc_f16(bool bf16, int M, int N) {
 
 size_t f16_slab_bytes(int bn) { return sizeof(float) * f16::ROWS * bn; }
 int f16_stage_k() { return f16::BKS; }
-int f16_epilogue_warps() { return f16::EPI_WARPS; }
+int f16_epilogue_warps(int bn) {
+  return bn == 512 ? f16::Cfg<2, 512>::EPI_WARPS : f16::Cfg<2, 256>::EPI_WARPS;
+}
 
 // Per-device setup of kernel (CG, BN) on the CURRENT device (the caller holds the
 // device-state mutex and records that it ran): the dynamic-smem / cluster-size
@@ -885,7 +901,7 @@ static cudaError_t prepare_cg(int sms, int* units) {
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(static_cast<unsigned>(sms - sms % 2));
-    cfg.blockDim = dim3(f16::NUM_THREADS);
+    cfg.blockDim = dim3(K::NUM_THREADS);
     cfg.dynamicSmemBytes = K::alloc;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -897,7 +913,7 @@ static cudaError_t prepare_cg(int sms, int* units) {
     return cudaOccupancyMaxActiveClusters(units, kern, &cfg);
   }
   int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, f16::NUM_THREADS, K::alloc);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, K::NUM_THREADS, K::alloc);
   *units = per_sm * sms;
   return e;
 }
@@ -913,7 +929,7 @@ static cudaError_t launch_cg(int cluster, const CUtensorMap& a, const CUtensorMa
   auto kern = f16::sk_gemm_f16<CG, BN, CF>;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(pairs_or_ctas * CG));
-  cfg.blockDim = dim3(f16::NUM_THREADS);
+  cfg.blockDim = dim3(f16::Cfg<CG, BN>::NUM_THREADS);
   cfg.dynamicSmemBytes = f16::Cfg<CG, BN>::alloc;
   cfg.stream = stream;
   cudaLaunchAttribute attr[2];
@@ -952,7 +968,7 @@ static cudaError_t cluster_capacity_cg(int cluster, int sms, int* clusters) {
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(sms - sms % cluster));
-  cfg.blockDim = dim3(f16::NUM_THREADS);
+  cfg.blockDim = dim3(f16::Cfg<CG, 256>::NUM_THREADS);
   cfg.dynamicSmemBytes = f16::Cfg<CG, 256>::alloc;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;

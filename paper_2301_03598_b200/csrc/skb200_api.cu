@@ -31,7 +31,7 @@ namespace skb200 {
 uint32_t make_idesc_f16(bool bf16, int M, int N);
 size_t f16_slab_bytes(int bn);
 int f16_stage_k();
-int f16_epilogue_warps();
+int f16_epilogue_warps(int bn);
 cudaError_t f16_prepare(int cg, int bn, int sms, int* units);
 cudaError_t f16_cluster_capacity(int cg, int cluster, int sms, int* clusters);
 cudaError_t launch_f16(int cg, int bn, int cluster, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
@@ -1244,7 +1244,7 @@ sk_status execute_pipelined(ExecCache& X, sk_gemm_desc& d, size_t ws_bytes, cons
   pf.np = static_cast<int>((cols + pf.w - 1) / pf.w);
   const int64_t groups = (rows + pf.g - 1) / pf.g, blocks = groups * pf.np;
   // stores per tile: one per epilogue warp of each CTA of the pair (tcgen05), one (DMMA)
-  const uint32_t incr = f64 ? 1u : static_cast<uint32_t>(kernel_ranks(kern) * f16_epilogue_warps());
+  const uint32_t incr = f64 ? 1u : static_cast<uint32_t>(kernel_ranks(kern) * f16_epilogue_warps(kernel_bn(kern)));
   std::vector<uint32_t> target(static_cast<size_t>(blocks), 0);
   std::vector<int64_t> firstA(static_cast<size_t>(rows), INT64_MAX), firstB(static_cast<size_t>(pf.np), INT64_MAX);
   std::vector<int64_t> lastC(static_cast<size_t>(blocks), -1);
