@@ -613,43 +613,46 @@ __global__ void __launch_bounds__(Cfg<CG, BN>::NUM_THREADS, 1)
           ptx::mbar_wait_cluster(xfix_bar, 0);
           const long long t_ready = ev ? static_cast<long long>(ptx::globaltimer()) : 0;
           const bool rows_in = m0 + static_cast<int32_t>(q * 32) < s.m;
-#pragma unroll 1
-          for (int cb = 0; rows_in && cb < jn / 8; ++cb) {
-            const int jb = j0 + cb * 8;  // first column group of this 32-column chunk
-            if (n0 + jb * 4 >= s.n) break;
-            float4 a[8];
-            // 16 columns of up to 4 contributors in flight per batch, folded in y order
+          // The fold is DSMEM-latency-bound: each thread's share (64/S column
+          // groups x S contributors = 64 float4) is read in two batches of 32
+          // loads in flight, folded in y order (owner first), then stored.
+          auto fold = [&](auto s_const) {
+            constexpr int SS = decltype(s_const)::value;
+            constexpr int GPB = 32 / SS;  // column groups per batch
+            uint32_t base[SS];
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-#pragma unroll 1
-              for (int y0 = 0; y0 < S; y0 += 4) {
-                float4 w[4][4];
+            for (int y = 0; y < SS; ++y) base[y] = mapa(park, static_cast<uint32_t>((SS - 1 - y) * CG) + hr);
+            float4 a[GPB < 8 ? 8 : GPB];
 #pragma unroll
-                for (int b = 0; b < 4; ++b) {
-                  if (y0 + b < S) {
-                    const uint32_t base = mapa(park, static_cast<uint32_t>((S - 1 - (y0 + b)) * CG) + hr);
+            for (int b = 0; b < 2; ++b) {
+              const int gb = j0 + b * GPB;  // first column group of this batch
+              float4 w[SS][GPB];
 #pragma unroll
-                    for (int j = 0; j < 4; ++j)
-                      w[b][j] = ptx::ld_dsmem_f4(base + ((jb + 4 * h + j) * ROWS + row) * 16);
-                  }
+              for (int y = 0; y < SS; ++y)
+#pragma unroll
+                for (int g = 0; g < GPB; ++g) w[y][g] = ptx::ld_dsmem_f4(base[y] + ((gb + g) * ROWS + row) * 16);
+              float4* dst = GPB < 8 ? a + b * GPB : a;
+#pragma unroll
+              for (int g = 0; g < GPB; ++g) {
+                float4 x = w[0][g];
+#pragma unroll
+                for (int y = 1; y < SS; ++y) {
+                  x.x += w[y][g].x; x.y += w[y][g].y; x.z += w[y][g].z; x.w += w[y][g].w;
                 }
+                dst[g] = x;
+              }
+              if (GPB >= 8) {  // whole 32-column chunks: store them now
 #pragma unroll
-                for (int b = 0; b < 4; ++b) {
-                  if (y0 + b < S) {
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                      float4& x = a[4 * h + j];
-                      if (y0 + b == 0) {
-                        x = w[b][j];
-                      } else {
-                        x.x += w[b][j].x; x.y += w[b][j].y; x.z += w[b][j].z; x.w += w[b][j].w;
-                      }
-                    }
-                  }
-                }
+                for (int cc = 0; cc < GPB / 8; ++cc)
+                  if (n0 + (gb + 8 * cc) * 4 < s.n) store_box(reinterpret_cast<const float*>(a + 8 * cc), n0, m0, (gb + 8 * cc) / 8);
               }
             }
-            store_box(reinterpret_cast<const float*>(a), n0, m0, jb / 8);
+            if (GPB < 8 && n0 + j0 * 4 < s.n) store_box(reinterpret_cast<const float*>(a), n0, m0, j0 / 8);
+          };
+          if (rows_in) {
+            if (S == 2) fold(std::integral_constant<int, 2>{});
+            else if (S == 4) fold(std::integral_constant<int, 4>{});
+            else fold(std::integral_constant<int, 8>{});
           }
           if (leader && rank == 0 && P.trace) {  // ownership / partial counts as the reference's protocol
             if (partial) {
