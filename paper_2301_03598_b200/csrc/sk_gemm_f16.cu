@@ -12,25 +12,33 @@
 //                                        ascending id) -> swizzled smem -> TMA store
 //   worker loop (:187-193)            -> persistent grid (sk_kernel_common.cuh)
 //
-// Two variants, one tile config each:
-//   CG = 1: 1-SM,  tile 128x256x64, tcgen05.mma.cta_group::1 M=128 N=256, grid = #SMs
-//   CG = 2: 2-SM,  tile 256x256x64, tcgen05.mma.cta_group::2 M=256 N=256 on a CTA
-//           pair (cluster of 2), grid = #SMs/2 pairs.  Each CTA of the pair loads
-//           its own 128 rows of A and its own 128 columns of B; the leader issues
-//           the MMA for both and every CTA drains its own 128 TMEM lanes.
+// Kernels (sk_gemm_f16<CG, BN, CF>), one tile config each:
+//   CG = 1, BN = 256: 1-SM, tile 128x256x64, tcgen05.mma.cta_group::1 M=128 N=256,
+//           grid = #SMs
+//   CG = 2, BN = 256: 2-SM, tile 256x256x64, tcgen05.mma.cta_group::2 M=256 N=256 on
+//           a CTA pair (cluster ranks 2i, 2i+1), grid = #SMs/2 pairs.  Each CTA of
+//           the pair loads its own 128 rows of A and its own 128 columns of B; the
+//           leader issues the MMA for both and every CTA drains its own 128 lanes.
+//   CG = 2, BN = 512: the wide 2-SM tile 256x512x64: two N=256 MMAs per k step
+//           share each A stage (48 instead of 64 B of operands per SM per MAC
+//           step); one 512-column TMEM accumulator, handed back by halves.
+//   CF = true (BN = 256): the cluster-fixup instantiation for fixed_split(S)
+//           launches whose t*S units fit as clusters of S units: a tile's S
+//           k-chunks reduce through DSMEM inside their cluster.
 //
 // Warp roles (192 threads, 1 CTA per SM):
 //   warp 0      TMA producer (one lane)
 //   warp 1      TMEM allocator + tcgen05.mma issuer (one lane; leader CTA only for CG=2)
 //   warps 2..5  epilogue; warp w drains TMEM lanes 32*(w%4) .. +31
 // Smem ring: STAGES k-blocks of A (rows x 64, K-major, 128B swizzle) and B
-// (64 x cols as 64x64 boxes, MN-major, 128B swizzle).  TMEM: two 256-column
-// fp32 accumulators, so one segment's epilogue overlaps the next mainloop.
-// All roles walk the same SegmentIter sequence (sk_kernel_common.cuh); tile ids
-// denote C blocks through Schedule::tile_rc (grouped rows).  Fixup: the owner
-// folds its peers (executor.hpp order), or -- schedules of >= 8 contributors per
-// tile, one unit per CTA -- every contributor publishes and folds a column
-// share (coop_fold).  Pieces of a tile outside C are skipped throughout.
+// (64 x cols as 64x64 boxes, MN-major, 128B swizzle).  TMEM (BN = 256): two
+// 256-column fp32 accumulators, so one segment's epilogue overlaps the next
+// mainloop.  All roles walk the same SegmentIter sequence (sk_kernel_common.cuh);
+// tile ids denote C blocks through Schedule::tile_rc (the reference's row-major
+// map unless grouped ids are requested).  Fixup: the owner folds its peers
+// (executor.hpp order); schedules of >= 8 contributors per tile, one unit per
+// CTA: every contributor publishes and folds a column share (coop_fold); the
+// cluster fixup above.  Pieces of a tile outside C are skipped throughout.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
