@@ -107,6 +107,38 @@ class ControlPlane:
 CPU_ROWS = {"bf16": 1024, "fp16": 1024, "fp64": 512}
 
 
+def fp64_leg(sk, torch, timed, p_dev_fp64, size=8192):
+    """8192^3 FP64 on the DMMA kernel: two_tile_sk_dp(p) and data-parallel
+    against cuBLAS DGEMM on the same operands (best of 3 bursts of 5 launches
+    each), then the config-4 sweep's stream_k:auto vs data-parallel geomean."""
+    from paper_2301_03598_b200 import sweep as sw
+
+    ab = sk.DType.Float64
+    blk = sk.kernel_blocking(ab)
+    pr = sk.GemmProblem(size, size, size)
+    A = sk.random_matrix_device(size, size, 42, sk.DType.Float64, ab)
+    B = sk.random_matrix_device(size, size, 43, sk.DType.Float64, ab)
+    Cd = torch.empty(size, size, device="cuda", dtype=torch.float64)
+    flops = 2.0 * size ** 3
+    out = {"shape": [size, size, size], "blocking": [blk.blk_m, blk.blk_n, blk.blk_k]}
+    for name, a in (("two_tile_sk_dp", sk.hybrid(pr, blk, p_dev_fp64, sk.HybridVariant.TwoTileSkDp)),
+                    ("data_parallel", sk.data_parallel(pr, blk))):
+        g = sk.Gemm(a, ab)
+        ms = min(timed(lambda: g.run(A, B, Cd), 5, 2) for _ in range(3))
+        g.check()
+        out[name] = {"ms": ms, "tflops": flops / (ms * 1e-3) / 1e12}
+    ms_c = min(timed(lambda: torch.matmul(A, B), 5, 2) for _ in range(3))
+    out["cublas_dgemm_tflops"] = flops / (ms_c * 1e-3) / 1e12
+    out["frac_of_cublas_dgemm"] = out["two_tile_sk_dp"]["tflops"] / out["cublas_dgemm_tflops"]
+    del A, B, Cd
+    rows = sw.run(sw.CONFIG4, ["data_parallel", "stream_k:auto"], sk.Variant.Auto, "fp64")
+    summ = sw.summarise(rows)["stream_k:auto"]
+    out["config4"] = {"shapes": len(sw.CONFIG4), "policy": "stream_k:auto",
+                      "geomean_sk_vs_dp": summ["geomean_speedup"], "min": summ["min"],
+                      "max": summ["max"], "regress_gt_5pct": summ["regress_gt_5pct"]}
+    return out
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -485,6 +517,14 @@ def main():
                      "gbps": round(r["gbps"], 1), "frac_of_hbm_peak": round(r["gbps"] / hbm, 3)}
                     for r in srows]
 
+    # BASELINE config 4 in the default run: FP64 DGEMM on the DMMA kernel (the
+    # paper's 64x64x16 tile), 8192^3 hybrid vs data-parallel vs cuBLAS DGEMM in
+    # this harness (the FP64 denominator: MEASURED_PEAKS.json has none), and the
+    # config-4 shapes' Stream-K policy vs data-parallel.
+    fp64 = None
+    if rank == 0 and not args.no_sweep and args.dtype != "fp64":
+        fp64 = fp64_leg(sk, torch, timed, p_dev_fp64=2 * sms)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         tf, dt, sample, cores, kind = cpu_reference_leg(args, int(strategy), param,
@@ -526,6 +566,7 @@ def main():
             "e2e": e2e,
             "cpu_baseline": cpu,
             "stream_k_vs_dp": sweep,
+            "fp64_config4": fp64,
         }
         print(json.dumps(line), flush=True)
     cp.close()

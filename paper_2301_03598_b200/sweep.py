@@ -22,9 +22,11 @@ columns: policy label, knob, kernel variant, dtype, timing copies / L2 state,
 TFLOP/s, GB/s, and the verification of that row's C (below) with the reference
 CPU executor's own time on the same WorkAssignment.
 
-Timing: each (shape, strategy) runs as a CUDA graph of R launches cycling over
-R operand copies (R chosen so the copies exceed L2 where memory allows), best
-of 3 replays, CUDA events on the capture stream.  Operands are the reference's
+Timing: each (shape, strategy) runs as a CUDA graph of L >= 8 launches (a multiple of R)
+cycling over R operand copies (R chosen so the copies exceed L2 where memory
+allows; a copy is re-read only after the others have streamed through L2), best
+of 3 replays, CUDA events on the capture stream.  L >= 8 keeps the graph's own
+start-up latency out of the per-launch time of large shapes, where R is 2.  Operands are the reference's
 random_matrix<float>(seed), (seed + 1) (matrix.hpp:56-68), generated on the
 device (sk_random_matrix) and rounded to the kernel's input type.
 
@@ -151,7 +153,7 @@ class ShapeTimer:
     """Pitched operand copies for one shape (the reference's random_matrix
     inputs, generated on the device) + graph-timed launches."""
 
-    def __init__(self, torch, m, n, k, dtype, seed, max_copies=16, mem_budget=4 << 30):
+    def __init__(self, torch, m, n, k, dtype, seed, max_copies=16, mem_budget=4 << 30, min_launches=8):
         self.torch = torch
         ab = _ab(dtype)
         fp64 = dtype == "fp64"
@@ -164,6 +166,9 @@ class ShapeTimer:
         self.copies = int(max(1, min(max_copies, math.ceil(2 * L2_BYTES / foot),
                                      mem_budget // max(foot, 1))))
         self.cold = self.copies * foot > L2_BYTES
+        # launches per graph replay, cycling over the copies (a copy comes back
+        # only after the others -- more than L2 when cold -- have streamed through)
+        self.launches = self.copies * max(1, -(-min_launches // self.copies))
         gen = sk.DType.Float64 if fp64 else sk.DType.Float32
         self.A, self.B = [], []
         for i in range(self.copies):  # copy i: random_matrix(seed + 2i), (seed + 2i + 1)
@@ -180,7 +185,8 @@ class ShapeTimer:
         s = torch.cuda.Stream()
         with torch.cuda.stream(s):
             with torch.cuda.graph(graph, stream=s):
-                for i in range(self.copies):
+                for j in range(self.launches):
+                    i = j % self.copies
                     gemm.run(self.A[i], self.B[i], self.C)
         torch.cuda.synchronize()
         best = float("inf")
@@ -194,7 +200,7 @@ class ShapeTimer:
             graph.replay()
             e1.record()
             torch.cuda.synchronize()
-            best = min(best, e0.elapsed_time(e1) * 1e3 / self.copies)
+            best = min(best, e0.elapsed_time(e1) * 1e3 / self.launches)
             r += 1
         gemm.check()
         return best
