@@ -424,7 +424,8 @@ def main():
     host = None
     if rank == 0:
         hp = sk.GemmProblem(512, 512, 512)
-        hg = sk.Gemm(sk.stream_k(hp, blk, p_dev), ab, variant)
+        ha = sk.auto_stream_k(hp, blk, p_dev)  # the policy's pick for this shape
+        hg = sk.Gemm(ha, ab, variant)
         hA = sk.random_matrix_device(512, 512, 1, gen, ab)
         hB = sk.random_matrix_device(512, 512, 2, gen, ab)
         hC = torch.empty(512, 512, device="cuda", dtype=cdt)
@@ -439,7 +440,8 @@ def main():
         torch.cuda.synchronize()
         ms_small = timed(lambda: hg.run(hA, hB, hC), 200, 10)
         hg.check()
-        host = {"shape": [512, 512, 512], "strategy": f"stream_k({p_dev})",
+        host = {"shape": [512, 512, 512],
+                "strategy": f"stream_k:auto -> {sk.strategy_name(ha.strategy)}({ha.param})",
                 "host_us_per_call": host_us, "device_us_per_launch_back_to_back": ms_small * 1e3,
                 "path": "Gemm.run -> sk_gemm (ctypes), no CUDA graph"}
 
