@@ -199,7 +199,8 @@ typedef struct sk_cost_params {
    * costs like coop_peers + contributors / 8 serial peer folds, not peers - 1
    * (0 = the reference's model: the owner folds every peer). */
   double coop_peers;
-  /* > 0: the kernel's cluster fixup (fixed_split(S), S in {8, 4, 2}, the S
+  /* > 0: the kernel's cluster fixup (fixed_split(S), S in {8, 4, 3, 2}; the
+   * kernel runs any 2 <= S <= 8), the S
    * k-chunks of a tile reduced through DSMEM) is a candidate of
    * sk_select_schedule when every chunk is nonempty, the largest chunk has at
    * least this many iterations and t * S units are co-resident as clusters of S
@@ -269,7 +270,7 @@ sk_status sk_tile_block(const sk_gemm_desc* desc, int64_t tile, int64_t* tile_ro
  * attributes on first use. */
 sk_status sk_persistent_capacity(sk_dtype ab_type, sk_variant variant, int32_t device, int32_t* units);
 /* Units (CTAs of the 1-SM kernel, CTA pairs of the 2-SM kernel) co-resident
- * as clusters of `cluster` units (2, 4 or 8) on `device` (-1 = current): the
+ * as clusters of `cluster` units (2 to 8) on `device` (-1 = current): the
  * capacity of the cluster fixup, fixed_split(S) with t * S <= units. */
 sk_status sk_cluster_capacity(sk_variant variant, int32_t cluster, int32_t device, int32_t* units);
 /* Stream-ordered, asynchronous.  Does not synchronise. */

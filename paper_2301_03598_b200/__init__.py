@@ -575,7 +575,7 @@ def load_matrix(path: str, dtype: DType) -> np.ndarray:
 
 def cluster_capacity(cluster: int, variant: "Variant" = None, device: int = -1) -> int:
     """Units (1-SM: CTAs, 2-SM: CTA pairs) co-resident as clusters of `cluster`
-    units (2, 4, 8): fixed_split(S) runs the DSMEM cluster fixup when t * S fits."""
+    units (2 to 8): fixed_split(S) runs the DSMEM cluster fixup when t * S fits."""
     variant = Variant.TwoSM if variant is None else variant
     out = C.c_int32()
     _check(lib().sk_cluster_capacity(int(variant), cluster, device, C.byref(out)), "cluster_capacity")

@@ -256,7 +256,11 @@ sk_status sk_select_schedule(const sk_cost_params* c, const sk_tile_grid_t* g, i
   // (1-SM) / >= 16 (2-SM pair) iterations it beat the model's pick and
   // data-parallel on ~95 % of such shapes, with no shape > 5 % slower than DP.
   if (c->cluster_min_iters > 0.0) {
-    for (int64_t S : {8, 4, 2}) {
+    // S = 5, 6, 7 run (the kernel folds whole 32-column boxes, 1-2 per slot)
+    // but measured no faster than S = 4 in geomean and up to 10 % slower on
+    // the 1-SM kernel; S = 3 beat S = 2 on every sampled shape (1.12-1.14x,
+    // profiles/r02z4/).  Candidates: the largest of 8, 4, 3, 2 that fits.
+    for (int64_t S : {8, 4, 3, 2}) {
       const int64_t ips = cdiv(g->iters_per_tile, S);
       if ((S - 1) * ips >= g->iters_per_tile) continue;  // an empty chunk: no cluster fixup
       if (static_cast<double>(ips) < c->cluster_min_iters) continue;

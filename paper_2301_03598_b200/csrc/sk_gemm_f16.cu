@@ -22,9 +22,9 @@
 //   CG = 2, BN = 512: the wide 2-SM tile 256x512x64: two N=256 MMAs per k step
 //           share each A stage (48 instead of 64 B of operands per SM per MAC
 //           step); one 512-column TMEM accumulator, handed back by halves.
-//   CF = true (BN = 256): the cluster-fixup instantiation for fixed_split(S)
-//           launches whose t*S units fit as clusters of S units: a tile's S
-//           k-chunks reduce through DSMEM inside their cluster.
+//   CF = true (BN = 256): the cluster-fixup instantiation for fixed_split(S),
+//           2 <= S <= 8, launches whose t*S units fit as clusters of S units: a
+//           tile's S k-chunks reduce through DSMEM inside their cluster.
 //
 // Warp roles (192 threads, 1 CTA per SM):
 //   warp 0      TMA producer (one lane)
@@ -599,7 +599,7 @@ __global__ void __launch_bounds__(Cfg<CG, BN>::NUM_THREADS, 1)
           const uint32_t cr = cluster_rank();
           const uint32_t slot = cr / CG, hr = cr % CG;
           float4* park = reinterpret_cast<float4*>(smem);
-          const int jn = (BN / 4) / S, j0 = static_cast<int>(slot) * jn;
+          const int jn = (BN / 4) / S, j0 = static_cast<int>(slot) * jn;  // S = 2, 4, 8
 #pragma unroll 1
           for (int c = 0; c < BN / 32; c += 2) {
             float v[64];
@@ -657,10 +657,52 @@ __global__ void __launch_bounds__(Cfg<CG, BN>::NUM_THREADS, 1)
             }
             if (GPB < 8 && n0 + j0 * 4 < s.n) store_box(reinterpret_cast<const float*>(a), n0, m0, j0 / 8);
           };
+          // S = 3, 5, 6, 7: slot i folds the whole 32-column boxes
+          // [i * 8 / S, (i + 1) * 8 / S) (1-3 boxes; the same boxes the
+          // power-of-two split gives for S = 2, 4, 8), one box (S <= 4) or half
+          // a box (S > 4) of all S contributors in flight per batch.
+          auto fold_boxes = [&](auto s_const) {
+            constexpr int SS = decltype(s_const)::value;
+            constexpr int GPB = SS <= 4 ? 8 : 4;  // column groups per batch: <= 32 loads in flight
+            uint32_t base[SS];
+#pragma unroll
+            for (int y = 0; y < SS; ++y) base[y] = mapa(park, static_cast<uint32_t>((SS - 1 - y) * CG) + hr);
+            const int bx0 = static_cast<int>(slot) * (BN / 32) / SS;
+            const int bx1 = (static_cast<int>(slot) + 1) * (BN / 32) / SS;
+#pragma unroll 1
+            for (int bx = bx0; bx < bx1 && n0 + bx * 32 < s.n; ++bx) {
+              float4 a[8];
+#pragma unroll
+              for (int h = 0; h < 8 / GPB; ++h) {
+                const int gb = bx * 8 + h * GPB;
+                float4 w[SS][GPB];
+#pragma unroll
+                for (int y = 0; y < SS; ++y)
+#pragma unroll
+                  for (int g = 0; g < GPB; ++g) w[y][g] = ptx::ld_dsmem_f4(base[y] + ((gb + g) * ROWS + row) * 16);
+#pragma unroll
+                for (int g = 0; g < GPB; ++g) {
+                  float4 x = w[0][g];
+#pragma unroll
+                  for (int y = 1; y < SS; ++y) {
+                    x.x += w[y][g].x; x.y += w[y][g].y; x.z += w[y][g].z; x.w += w[y][g].w;
+                  }
+                  a[h * GPB + g] = x;
+                }
+              }
+              store_box(reinterpret_cast<const float*>(a), n0, m0, bx);
+            }
+          };
           if (rows_in) {
-            if (S == 2) fold(std::integral_constant<int, 2>{});
-            else if (S == 4) fold(std::integral_constant<int, 4>{});
-            else fold(std::integral_constant<int, 8>{});
+            switch (S) {
+              case 2: fold(std::integral_constant<int, 2>{}); break;
+              case 3: fold_boxes(std::integral_constant<int, 3>{}); break;
+              case 4: fold(std::integral_constant<int, 4>{}); break;
+              case 5: fold_boxes(std::integral_constant<int, 5>{}); break;
+              case 6: fold_boxes(std::integral_constant<int, 6>{}); break;
+              case 7: fold_boxes(std::integral_constant<int, 7>{}); break;
+              default: fold(std::integral_constant<int, 8>{}); break;
+            }
           }
           if (leader && rank == 0 && P.trace) {  // ownership / partial counts as the reference's protocol
             if (partial) {

@@ -94,7 +94,8 @@ struct DeviceInfo {
   // becomes resident, so every launch is capped by it.
   bool f16_ready[3] = {false, false, false};  // per tcgen05 kernel (Kernel enum order)
   int f16_units[3] = {0, 0, 0};
-  int cluster_caps[2][4] = {{-1, -1, -1, -1}, {-1, -1, -1, -1}};  // [cg - 1][S = 2, 4, 8]: clusters
+  int cluster_caps[2][9] = {{-1, -1, -1, -1, -1, -1, -1, -1, -1},
+                            {-1, -1, -1, -1, -1, -1, -1, -1, -1}};  // [cg - 1][S = 2..8]: clusters
   bool f64_ready = false;
   int f64_per_sm = 0;
 };
@@ -916,10 +917,9 @@ sk_status resident_units(int dev, const DeviceInfo& info, Kernel kern, int* out)
 // holds no lock; resident_units() has set the kernel's attributes.
 int cluster_units(int dev, const DeviceInfo& info, Kernel kern, int S) {
   const int cg = kernel_cg(kern);
-  const int slot = S == 2 ? 1 : S == 4 ? 2 : 3;
   std::lock_guard<std::mutex> lk(g_dev_mu);
   DeviceInfo& di = g_dev[dev];
-  int& cap = di.cluster_caps[cg - 1][slot];
+  int& cap = di.cluster_caps[cg - 1][S];
   if (cap < 0) {
     int c = 0;
     if (f16_cluster_capacity(cg, S * cg, info.sms, &c) != cudaSuccess) {
@@ -931,8 +931,8 @@ int cluster_units(int dev, const DeviceInfo& info, Kernel kern, int S) {
   return cap * S;
 }
 
-// Cluster fixup (256-wide tcgen05 kernels, fixed_split(S)): usable when S is 2,
-// 4 or 8, no k-chunk is empty (every unit of a cluster has a segment: the
+// Cluster fixup (256-wide tcgen05 kernels, fixed_split(S)): usable when
+// 2 <= S <= 8, no k-chunk is empty (every unit of a cluster has a segment: the
 // last chunk [(S-1) ips, ipt) is nonempty) and all t * S units are co-resident
 // as clusters of S units.
 int cluster_fix_for(int dev, const DeviceInfo& info, Kernel kern, const Schedule& s) {
@@ -940,7 +940,7 @@ int cluster_fix_for(int dev, const DeviceInfo& info, Kernel kern, const Schedule
       knobs().cluster_fix == 0)
     return 0;
   const int64_t S = s.split;
-  if ((S != 2 && S != 4 && S != 8) || (S - 1) * s.ips >= s.ipt) return 0;
+  if (S < 2 || S > 8 || (S - 1) * s.ips >= s.ipt) return 0;
   return s.grid_size <= cluster_units(dev, info, kern, static_cast<int>(S)) ? static_cast<int>(S) : 0;
 }
 
@@ -1590,7 +1590,7 @@ extern "C" void sk_execute_release(void) { g_exec.release(); }
 
 extern "C" sk_status sk_cluster_capacity(sk_variant variant, int32_t cluster, int32_t device,
                                          int32_t* units) {
-  if (!units || (cluster != 2 && cluster != 4 && cluster != 8)) return fail(SK_EINVAL, "clusters of 2, 4 or 8 units");
+  if (!units || cluster < 2 || cluster > 8) return fail(SK_EINVAL, "clusters of 2 to 8 units");
   if (variant != SK_VARIANT_1SM && variant != SK_VARIANT_2SM)
     return fail(SK_EUNSUPPORTED, "the cluster fixup runs on the 1-SM and 2-SM 256-wide kernels");
   *units = 0;

@@ -514,7 +514,9 @@ def test_cooperative_fixup_bit_exact(sk, port, torch_cuda, monkeypatch, shape, g
 @pytest.mark.parametrize("var", ["1sm", "2sm"])
 @pytest.mark.parametrize("shape,s", [((128, 8192, 8192), 4), ((128, 8192, 8192), 2), ((129, 264, 1024), 2),
                                      ((129, 264, 1024), 8), ((256, 512, 4096), 8), ((1000, 1000, 512), 2),
-                                     ((64, 328, 2048), 4), ((300, 1000, 1000), 4)])
+                                     ((64, 328, 2048), 4), ((300, 1000, 1000), 4),
+                                     ((129, 264, 1024), 3), ((64, 328, 2048), 5), ((256, 512, 4096), 6),
+                                     ((200, 600, 2048), 7), ((128, 4096, 16384), 7)])
 def test_cluster_fixup_fixed_split(sk, port, torch_cuda, monkeypatch, shape, s, var):
     """fixed_split(s) with no empty k-chunk runs the cluster fixup when t * s
     units fit as clusters (the s k-chunks of a tile on one cluster, reduced
@@ -549,6 +551,14 @@ def test_cluster_fixup_fixed_split(sk, port, torch_cuda, monkeypatch, shape, s, 
             outs[on, name] = C.cpu().numpy()
         storers = gemm.block_storers()
         assert np.array_equal(storers.reshape(-1), np.array(owners)), on
+        if on == "1" and a.grid.total_tiles * s <= sk.cluster_capacity(s, V):
+            # the cluster path ran: every unit's record carries S - 1 (partials
+            # included; the global-slab path records 0 peers for a partial)
+            tl = sk.Gemm(a, variant=V, timeline=True)
+            tl.run(A, B, C)
+            tl.check()
+            kinds = tl.timeline()[:, 3].astype(np.int64)
+            assert np.all(((kinds >> 8) & 0xFF) == s - 1), kinds[:8]
     monkeypatch.undo()
     sk.reload_env()
     assert np.array_equal(outs["1", "int"], want)

@@ -227,16 +227,23 @@ def test_cluster_capacity_and_policy(sk, torch_cuda, checker, var):
     torch = torch_cuda
     V = sk.Variant.OneSM if var == "1sm" else sk.Variant.TwoSM
     p = 148 if var == "1sm" else 74
-    caps = {S: sk.cluster_capacity(S, V) for S in (2, 4, 8)}
+    caps = {S: sk.cluster_capacity(S, V) for S in range(2, 9)}
     assert all(0 <= caps[S] <= p and caps[S] % S == 0 for S in caps), caps
     assert caps[2] > 0
     blk = sk.kernel_blocking(sk.DType.BFloat16, V)
-    m, n, k = 128, 8192, 8192  # 32 tiles of 128 iterations
+    min_iters = sk.default_cost_params(variant=V).cluster_min_iters
+    # 32, 16, 20, 40 tiles on the 1-SM kernel (128 x 10240: S = 3 when 4 does not fit)
+    for m, n, k in ((128, 8192, 8192), (128, 4096, 16384), (64, 5120, 8192), (128, 10240, 8192)):
+        a = sk.auto_stream_k(sk.GemmProblem(m, n, k), blk, p)
+        t, ipt = a.grid.total_tiles, a.grid.iters_per_tile
+        want_s = next((S for S in (8, 4, 3, 2) if t * S <= caps[S] and -(-ipt // S) >= min_iters
+                       and (S - 1) * -(-ipt // S) < ipt), None)
+        if want_s is None:
+            assert a.strategy != sk.Strategy.FixedSplit, (m, n, k, caps)
+        else:
+            assert (a.strategy, a.param) == (sk.Strategy.FixedSplit, want_s), (m, n, k, caps)
+    m, n, k = 128, 8192, 8192
     a = sk.auto_stream_k(sk.GemmProblem(m, n, k), blk, p)
-    t = a.grid.total_tiles
-    want_s = next((S for S in (8, 4, 2) if t * S <= caps[S] and 128 // S >= 8), None)
-    assert want_s is not None
-    assert (a.strategy, a.param) == (sk.Strategy.FixedSplit, want_s)
     bw = sk.kernel_blocking(sk.DType.BFloat16, sk.Variant.TwoSMWide)
     aw = sk.auto_stream_k(sk.GemmProblem(m, n, k), bw, 74, sk.default_cost_params(variant=sk.Variant.TwoSMWide))
     assert aw.strategy != sk.Strategy.FixedSplit
