@@ -1,5 +1,5 @@
 set -u
-O=gpurun_out/final
+O=gpurun_out/${1:-final}
 mkdir -p $O
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo rc=$? >> $O/smoke.log
 timeout 1500 python -m pytest tests -m gpu -q > $O/pytest.log 2>&1; echo rc=$? >> $O/pytest.log
