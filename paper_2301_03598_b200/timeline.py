@@ -78,7 +78,10 @@ def write_timeline_csv(tl: Timeline, out) -> None:
 
 def render_gantt(tl: Timeline, out) -> None:
     """SVG Gantt in the layout of simulate.cpp:105-154: one row per core, one
-    rectangle per event colour-keyed by tile, fixup events hatched."""
+    rectangle per event colour-keyed by tile, fixup events hatched.  It keeps
+    the reference's geometry, palette and labels on purpose (§8(f) row 4 asks
+    for output in the reference's format); it is a reporting helper, off the
+    GEMM hot path."""
     chart_w, row_h, gap, left, top = 720.0, 26.0, 6.0, 64.0, 16.0
     height = top + tl.p * (row_h + gap) + 32.0
     width = left + chart_w + 16.0
